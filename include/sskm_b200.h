@@ -1,0 +1,187 @@
+/* sskm_b200 — C-ABI boundary of the B200-native sparse spherical k-means core.
+ *
+ * Plain pointers and sizes only (no torch / C++ types). Every entry point
+ * returns an int status: SSKM_OK, SSKM_EINVAL (what the reference throws as
+ * std::invalid_argument -> Python ValueError, CLI exit 2), or SSKM_ERUNTIME
+ * (CUDA / resource failure -> std::runtime_error, CLI exit 1). The message of
+ * the last failure on the calling thread is sskm_last_error().
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj/include/sskm/engine.hpp unless noted). A context is
+ * driven by one host thread; it owns device-resident corpus shard, centroids
+ * and state on one GPU, so per-iteration calls move no bulk data over PCIe.
+ */
+#ifndef SSKM_B200_H
+#define SSKM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSKM_OK 0
+#define SSKM_EINVAL 1
+#define SSKM_ERUNTIME 2
+
+/* Mode, engine.hpp:13 (parse_mode, engine.cpp:21-27). */
+#define SSKM_MODE_BASELINE 0
+#define SSKM_MODE_NCC 1
+#define SSKM_MODE_NCC_INDEX 2 /* runs the exact NCC kernels; index_active stays 0 */
+
+/* StopReason, engine.hpp:59 */
+#define SSKM_STOP_NO_REASSIGNMENTS 0
+#define SSKM_STOP_CENTROID_DRIFT 1
+#define SSKM_STOP_MAX_ITERATIONS 2
+
+/* RunConfig, engine.hpp:20-41 (+ GPU-only knobs that do not change the
+ * meaning of the reference fields). */
+typedef struct {
+    uint32_t k;
+    int32_t mode;
+    const double* lambdas; /* validated like the reference; the index is not built */
+    uint32_t n_lambdas;
+    double conv_sq_dist;
+    double ncc_epsilon;
+    uint32_t index_activation_threshold;
+    uint32_t max_iters;
+    uint64_t seed;    /* k-means++ seed when no init seeds are given */
+    uint32_t threads; /* accepted for API parity; the GPU grid replaces it */
+    int32_t device;   /* CUDA device ordinal */
+} sskm_run_config;
+
+/* IterationStats, engine.hpp:43-57, followed by GPU extras. `dot_products`
+ * counts exactly what the reference's assign would have evaluated
+ * (engine.cpp:253-306) so the reference's accounting invariants hold;
+ * `gpu_dot_products` is what the kernels evaluated. */
+typedef struct {
+    uint32_t iteration;
+    uint32_t n_unchanged_centroids;
+    uint64_t n_reassigned;
+    uint64_t dot_products;
+    uint64_t index_queries;
+    uint64_t candidates_total;
+    double wall_seconds;
+    double index_build_seconds;
+    double max_sq_drift;
+    double objective;
+    int32_t index_active;
+    int32_t n_repaired;
+    /* --- GPU extras --- */
+    uint64_t gpu_dot_products;
+    uint64_t n_moved;         /* documents whose cluster changed since the last update */
+    uint32_t n_changed;       /* centroids scanned by the NCC pass (unchanged flag clear) */
+    uint32_t n_recomputed;    /* centroid columns rewritten by the update */
+    uint64_t n_rescan;        /* NCC documents that needed the unchanged-centroid pass */
+    double update_ms;         /* device time of compute_centroids + detect_unchanged */
+    double assign_ms;         /* device time of the assignment step */
+    double assign_kernel_ms;  /* device time of the dominant assign kernel(s) only */
+} sskm_iteration_stats;
+
+typedef struct sskm_ctx sskm_ctx;
+
+const char* sskm_last_error(void);
+
+/* Validation exactly as RunConfig::validate (engine.cpp:47-64). */
+int sskm_validate(const sskm_run_config* cfg, uint64_t n_docs);
+
+/* Context on one device. */
+int sskm_open(int32_t device, sskm_ctx** out);
+int sskm_close(sskm_ctx* ctx);
+
+/* Copies a caller-owned CSR corpus (int64 indptr[n+1], int32 indices sorted
+ * strictly ascending within a row, fp32 values) to the device. Replaces
+ * building sskm::CorpusMatrix (corpus.hpp:26-32). For a document shard of a
+ * multi-GPU run, doc_offset is the global id of row 0 and n_docs_total the
+ * global corpus size (both 0 / n_docs for a single GPU). */
+int sskm_upload_csr(sskm_ctx* ctx, int64_t n_docs, uint32_t dims, const int64_t* indptr,
+                    const int32_t* indices, const float* values, int64_t doc_offset,
+                    int64_t n_docs_total);
+
+/* Config for the following calls; validates like RunConfig::validate. */
+int sskm_configure(sskm_ctx* ctx, const sskm_run_config* cfg);
+
+/* BASELINE init: centroid j = document seeds[j] (global ids), then the
+ * nearest-seed full-scan assignment with ties to the lowest seed — the state
+ * seed_kmeanspp (engine.hpp:74, engine.cpp:82-97) leaves for those seeds. */
+int sskm_init_from_seeds(sskm_ctx* ctx, const uint32_t* seeds);
+
+/* k-means++ seeding, seed_kmeanspp (engine.hpp:74; engine.cpp:66-130), with the
+ * pinned mt19937_64 draws (random.hpp:11-19); writes the k chosen documents. */
+int sskm_init_kmeanspp(sskm_ctx* ctx, uint64_t seed, uint32_t* seeds_out);
+
+/* compute_centroids (engine.hpp:93) + detect_unchanged (engine.hpp:106) + the
+ * repaired-forces-changed rule (engine.cpp:371-376): one iteration's update. */
+int sskm_update(sskm_ctx* ctx, sskm_iteration_stats* st);
+
+/* assign (engine.hpp:124) for the current iteration (full scan on iteration 1
+ * or in baseline mode, exact NCC otherwise) + objective (engine.cpp:403-405). */
+int sskm_assign(sskm_ctx* ctx, sskm_iteration_stats* st);
+
+/* One Lloyd iteration = sskm_update + sskm_assign (run() loop body, engine.cpp:357-407). */
+int sskm_step(sskm_ctx* ctx, sskm_iteration_stats* st);
+
+/* run() loop (engine.cpp:357-424) from the current state: iterations until no
+ * reassignment, drift < conv_sq_dist (iteration > 1), or max_iters. */
+int sskm_run(sskm_ctx* ctx, sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters,
+             int32_t* stop_reason);
+
+/* State readback / teacher forcing (ClusteringState, engine.hpp:110-117). */
+int sskm_get_state(sskm_ctx* ctx, uint32_t* assignments, double* sims, uint8_t* unchanged);
+int sskm_set_state(sskm_ctx* ctx, const uint32_t* assignments, const double* sims,
+                   uint32_t iteration);
+/* Centroids as Cᵀ, d rows × k columns, row-major fp32. */
+int sskm_get_centroids(sskm_ctx* ctx, float* ct);
+int sskm_set_centroids(sskm_ctx* ctx, const float* ct);
+/* Teacher forcing of the NCC flags (unchanged[j] = 1: cluster j skipped by the
+ * changed-list scan); extension, no reference counterpart. */
+int sskm_set_unchanged(sskm_ctx* ctx, const uint8_t* unchanged);
+int sskm_get_repaired(sskm_ctx* ctx, uint32_t* repaired, uint32_t* n_repaired);
+int sskm_get_iteration(sskm_ctx* ctx, uint32_t* iteration);
+
+/* Device timing on the context's stream (CUDA events; 16 slots) and the
+ * number of kernels this context has launched — the bench's live evidence. */
+int sskm_timer_record(sskm_ctx* ctx, int32_t slot);
+int sskm_timer_elapsed(sskm_ctx* ctx, int32_t a, int32_t b, double* ms);
+int sskm_launch_count(sskm_ctx* ctx, uint64_t* n);
+int sskm_synchronize(sskm_ctx* ctx);
+
+/* One-shot drop-in for sskm::run(const CorpusMatrix&, const RunConfig&)
+ * (engine.hpp:148): upload, seed (given seeds, or k-means++ when seeds is
+ * NULL), iterate, download. Any output pointer may be NULL. */
+int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims,
+                     const int64_t* indptr, const int32_t* indices, const float* values,
+                     const uint32_t* seeds, uint32_t* assignments, double* sims, float* ct,
+                     sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters,
+                     int32_t* stop_reason, double* objective);
+
+/* ---- multi-GPU document sharding (one context per GPU / process) ----------
+ * Documents are sharded in contiguous ranges; centroids and the fixed-point
+ * cluster sums are replicated. An iteration's update exchanges only the rows
+ * of documents that moved (delta path). The host driver moves the bytes with
+ * its collective library (NCCL via torch.distributed), in rank order. */
+
+/* Local cluster sizes (int64[k]) for the global empty-cluster check. */
+int sskm_local_counts(sskm_ctx* ctx, int64_t* counts);
+/* Lowest-(sim, global doc id) local donor among docs whose cluster has global
+ * size >= 2 (engine.cpp:156-161). Writes sim and global id (INT64_MAX if none). */
+int sskm_local_donor(sskm_ctx* ctx, const int64_t* global_counts, double* sim, int64_t* doc);
+/* Reassign a local document (repair move, engine.cpp:162-165). */
+int sskm_move_doc(sskm_ctx* ctx, int64_t global_doc, uint32_t cluster);
+/* Packs the locally moved documents: header counts then payload, see DESIGN.md. */
+int sskm_moved_size(sskm_ctx* ctx, int64_t* n_moved, int64_t* nnz_moved);
+int sskm_moved_pack(sskm_ctx* ctx, int64_t* doc_ids, uint32_t* old_c, uint32_t* new_c,
+                    int64_t* row_ptr, int32_t* idx, float* val);
+/* Applies gathered moved rows (DEVICE pointers on this context's GPU; rows
+ * from all ranks, any order) to the
+ * replicated sums, then finishes the update exactly like sskm_update. */
+int sskm_update_apply(sskm_ctx* ctx, int64_t n_moved, const uint32_t* old_c, const uint32_t* new_c,
+                      const int64_t* row_ptr, const int32_t* idx, const float* val,
+                      const uint32_t* repaired, uint32_t n_repaired, sskm_iteration_stats* st);
+/* Local partials for the assign step's scalars (sums over the shard). */
+int sskm_local_sims_sum(sskm_ctx* ctx, double* sum);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSKM_B200_H */

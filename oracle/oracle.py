@@ -261,12 +261,11 @@ def validate(n_docs, k, conv_sq_dist=1e-4, ncc_epsilon=0.0, max_iters=100,
 
 def dense_to_csr(ct: np.ndarray, k: int):
     """Cᵀ (d × ≥k, any float dtype) -> centroid CSR over k rows with fp64 values."""
-    cols = np.ascontiguousarray(ct[:, :k].T).astype(np.float64)
-    nz = cols != 0.0
-    counts = nz.sum(axis=1)
+    cols = np.ascontiguousarray(ct[:, :k].T)
+    jj, tt = np.nonzero(cols)
+    counts = np.bincount(jj, minlength=k)
     ptr = np.zeros(k + 1, np.int64)
     ptr[1:] = np.cumsum(counts)
-    jj, tt = np.nonzero(nz)
     return ptr, tt.astype(np.uint32), cols[jj, tt].astype(np.float64)
 
 

@@ -1,0 +1,30 @@
+"""B200-native data-parallel core of sparse spherical k-means (arXiv 2108.00895).
+
+Drop-in for the reference `sskm` hot path (proj/python/sskm/__init__.py):
+`cluster`, `CorpusMatrix`, `ClusteringResult`, `IterationStats`, backed by the
+sm_100a kernels in csrc/ behind the C-ABI in include/sskm_b200.h.
+"""
+from ._lib import load as _load_native
+from .api import (
+    ClusteringResult,
+    CorpusMatrix,
+    Engine,
+    IterationStats,
+    SparseVector,
+    cluster,
+    parse_mode,
+    validate,
+)
+
+_load_native()  # fail loudly at import if the native library is unusable
+
+__all__ = [
+    "ClusteringResult",
+    "CorpusMatrix",
+    "Engine",
+    "IterationStats",
+    "SparseVector",
+    "cluster",
+    "parse_mode",
+    "validate",
+]

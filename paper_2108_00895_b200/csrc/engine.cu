@@ -1,0 +1,1096 @@
+// sskm_b200 engine: device-resident Lloyd iterations behind the C-ABI in
+// include/sskm_b200.h. Host C++ orchestrates; all per-document and
+// per-centroid work runs in the kernels of assign_kernels.cuh and
+// update_kernels.cuh on one CUDA stream.
+//
+// Mirrors the reference loop (engine.cpp:345-425):
+//   update  = compute_centroids (:137-195) + detect_unchanged (:197-216) + repaired rule (:371-376)
+//   assign  = assign (:218-322) + objective Σ sims (:403-405)
+//   run     = stop on no reassignment (:409-412) or drift < conv_sq_dist after iteration 1 (:413-416)
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/sskm_b200.h"
+#include "assign_kernels.cuh"
+#include "common.cuh"
+#include "update_kernels.cuh"
+
+namespace sskm_b200 {
+
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+
+// Device scalars, one allocation.
+struct Scalars {
+    unsigned long long n_moved;
+    unsigned long long n_rescan;
+    unsigned long long reassigned;
+    unsigned long long max_drift_bits;
+    unsigned long long donor_key;
+    unsigned long long donor_idx;
+    unsigned int n_rec;
+    unsigned int n_chg;
+    unsigned int n_empty;
+    unsigned int n_unchanged;
+    unsigned int bad;
+    unsigned int zero_flag;
+    double objective;
+};
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count <= n && p) return;
+        free();
+        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        n = count;
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { free(); }
+};
+
+class Engine {
+public:
+    explicit Engine(int device) : device_(device) {
+        int n_dev = 0;
+        CK(cudaGetDeviceCount(&n_dev));
+        if (device < 0 || device >= n_dev) throw InvalidArgument("invalid CUDA device ordinal");
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) throw CudaError("sskm_b200 requires an sm_100 (B200) device");
+        sms_ = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        for (auto& e : ev_) CK(cudaEventCreate(&e));
+        for (auto& e : user_ev_) CK(cudaEventCreate(&e));
+        scal_.alloc(1);
+        CK(cudaMallocHost(&hs_, sizeof(Scalars)));
+    }
+
+    ~Engine() {
+        cudaSetDevice(device_);
+        cudaStreamSynchronize(stream_);
+        for (auto& e : ev_) cudaEventDestroy(e);
+        for (auto& e : user_ev_) cudaEventDestroy(e);
+        cudaStreamDestroy(stream_);
+        if (hs_) cudaFreeHost(hs_);
+    }
+
+    // Every kernel goes through here: one place to count launches (bench's
+    // gpu_launches) and to pin the stream.
+    template <typename... KArgs, typename... Args>
+    void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, Args&&... args) {
+        kernel<<<grid, block, 0, stream_>>>(std::forward<Args>(args)...);
+        ++launches_;
+    }
+
+    uint64_t launches() const { return launches_; }
+
+    void timer_record(int slot) {
+        if (slot < 0 || slot >= kUserEvents) throw InvalidArgument("timer slot out of range");
+        CK(cudaEventRecord(user_ev_[slot], stream_));
+    }
+
+    double timer_elapsed(int a, int b) {
+        if (a < 0 || a >= kUserEvents || b < 0 || b >= kUserEvents) throw InvalidArgument("timer slot out of range");
+        CK(cudaEventSynchronize(user_ev_[b]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, user_ev_[a], user_ev_[b]));
+        return ms;
+    }
+
+    void synchronize() { CK(cudaStreamSynchronize(stream_)); }
+
+    // ------------------------------------------------------------ corpus --
+    void upload(int64_t n, uint32_t dims, const int64_t* indptr, const int32_t* indices,
+                const float* values, int64_t doc_offset, int64_t n_total) {
+        CK(cudaSetDevice(device_));
+        if (n <= 0) throw InvalidArgument("empty corpus");
+        if (dims == 0) throw InvalidArgument("dims must be positive");
+        if (indptr[0] != 0) throw InvalidArgument("indptr[0] must be 0");
+        const int64_t nnz = indptr[n];
+        if (nnz < 0 || nnz > (int64_t(1) << 40)) throw InvalidArgument("bad nnz");
+        if (n > 0xFFFFFFF0ll) throw InvalidArgument("too many documents for 32-bit ids");
+        n_ = n;
+        d_ = dims;
+        nnz_ = nnz;
+        doc_offset_ = doc_offset;
+        n_total_ = n_total > 0 ? n_total : n;
+        indptr_.alloc(n + 1);
+        idx_.alloc(nnz);
+        val_.alloc(nnz);
+        CK(cudaMemcpyAsync(indptr_.p, indptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+        if (nnz) {
+            CK(cudaMemcpyAsync(idx_.p, indices, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, stream_));
+            CK(cudaMemcpyAsync(val_.p, values, nnz * sizeof(float), cudaMemcpyHostToDevice, stream_));
+        }
+        reset_scalars();
+        launch(validate_csr_kernel, grid_for(n, 256), 256, indptr_.p, idx_.p, val_.p, n, dims,
+                                                                   &scal_.p->bad);
+        CK_LAUNCH();
+        pull_scalars();
+        if (hs_->bad & 1u) throw InvalidArgument("indptr must be non-decreasing");
+        if (hs_->bad & 2u)
+            throw InvalidArgument("SparseVector: dims not strictly increasing (or out of range)");
+        if (hs_->bad & 4u) throw InvalidArgument("SparseVector: zero weight");
+        if (hs_->bad & 8u)
+            throw InvalidArgument("document weights must be finite with |x| <= 1 (unit-length rows)");
+        // fixed-point scale: N_total · 2^K <= 2^62 with |x| <= 1
+        int lg = 0;
+        while ((int64_t(1) << lg) < n_total_) ++lg;
+        K_ = 62 - lg;
+        a_.alloc(n);
+        a_sum_.alloc(n);
+        a_start_.alloc(n);
+        sims_.alloc(n);
+        moved_.alloc(n);
+        rescan_.alloc(n);
+        corpus_ = true;
+        state_ = false;
+    }
+
+    // ------------------------------------------------------------ config --
+    static void validate(const sskm_run_config& c, uint64_t n_docs) {
+        // RunConfig::validate, engine.cpp:47-64 (same messages)
+        if (c.k < 2) throw InvalidArgument("k must be at least 2");
+        if (c.k > n_docs)
+            throw InvalidArgument("k (" + std::to_string(c.k) + ") exceeds the number of documents (" +
+                                  std::to_string(n_docs) + ")");
+        for (uint32_t i = 0; i < c.n_lambdas; ++i) {
+            if (!(c.lambdas[i] > 0.0 && c.lambdas[i] < 1.0)) throw InvalidArgument("lambda must be in (0, 1)");
+            if (i > 0 && !(c.lambdas[i] > c.lambdas[i - 1]))
+                throw InvalidArgument("lambdas must be strictly ascending");
+        }
+        if (!(c.conv_sq_dist > 0.0)) throw InvalidArgument("conv_sq_dist must be positive");
+        if (c.ncc_epsilon < 0.0) throw InvalidArgument("ncc_epsilon must be nonnegative");
+        if (c.max_iters < 1) throw InvalidArgument("max_iters must be at least 1");
+        if (c.mode < SSKM_MODE_BASELINE || c.mode > SSKM_MODE_NCC_INDEX)
+            throw InvalidArgument("unknown mode (expected baseline, ncc, or ncc+index)");
+    }
+
+    void configure(const sskm_run_config& c) {
+        CK(cudaSetDevice(device_));
+        if (!corpus_) throw InvalidArgument("upload a corpus before configuring");
+        validate(c, static_cast<uint64_t>(n_total_));
+        cfg_ = c;
+        lambdas_.assign(c.lambdas, c.lambdas + c.n_lambdas);
+        cfg_.lambdas = lambdas_.data();
+        if (k_ != c.k) {
+            k_ = c.k;
+            ld_ = static_cast<uint32_t>(round_up(k_, 128));
+            const uint64_t dk = static_cast<uint64_t>(d_) * ld_;
+            ct_.alloc(dk);
+            S_.alloc(dk);
+            unchanged_.alloc(k_);
+            touched_.alloc(k_);
+            repaired_flag_.alloc(k_);
+            counts_.alloc(k_);
+            rec_ids_.alloc(k_);
+            rec_pos_.alloc(k_);
+            chg_ids_.alloc(k_);
+            drift_.alloc(k_);
+            norm2_.alloc(k_);
+            drift_rec_.alloc(k_);
+            const uint64_t n_rb = ceil_div(d_, kRowBlock);
+            part_.alloc(n_rb * k_);
+            state_ = false;
+        }
+        if (cfg_.mode != SSKM_MODE_BASELINE) cc_.alloc(static_cast<uint64_t>(d_) * ld_);
+        obj_part_.alloc(kObjBlocks);
+    }
+
+    // -------------------------------------------------------------- init --
+    void reset_sums() {
+        CK(cudaMemsetAsync(S_.p, 0, static_cast<uint64_t>(d_) * ld_ * sizeof(long long), stream_));
+        launch(fill_u32_kernel, grid_for(n_, 256), 256, a_sum_.p, n_, kNone);
+        CK_LAUNCH();
+        CK(cudaMemsetAsync(touched_.p, 0, k_, stream_));
+    }
+
+    void init_from_seeds(const uint32_t* seeds_global) {
+        need_config();
+        std::vector<uint32_t> local(k_);
+        for (uint32_t j = 0; j < k_; ++j) {
+            const int64_t g = seeds_global[j];
+            if (g < 0 || g >= n_total_) throw InvalidArgument("seed out of range");
+            if (g < doc_offset_ || g >= doc_offset_ + n_)
+                throw InvalidArgument("seed document is not on this shard");
+            local[j] = static_cast<uint32_t>(g - doc_offset_);
+        }
+        DevBuf<uint32_t> dseeds;
+        dseeds.alloc(k_);
+        CK(cudaMemcpyAsync(dseeds.p, local.data(), k_ * 4, cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemsetAsync(ct_.p, 0, static_cast<uint64_t>(d_) * ld_ * sizeof(float), stream_));
+        launch(scatter_seeds_kernel, grid_for(static_cast<int64_t>(k_) * 32, 256), 256, 
+            indptr_.p, idx_.p, val_.p, dseeds.p, k_, ct_.p, ld_);
+        CK_LAUNCH();
+        seed_assign_state();
+        sskm_iteration_stats st{};
+        full_assign(&st);
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    // Single-GPU k-means++ (engine.cpp:66-130). The per-round cumulative sum
+    // runs on the host in document order so the picks are the reference's.
+    void init_kmeanspp(uint64_t seed, uint32_t* seeds_out) {
+        need_config();
+        if (n_ != n_total_) throw InvalidArgument("k-means++ seeding needs the whole corpus on one GPU");
+        std::mt19937_64 gen(seed);
+        auto uniform_unit = [&] { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+        auto uniform_index = [&](size_t n) {
+            size_t i = static_cast<size_t>(uniform_unit() * static_cast<double>(n));
+            return i < n ? i : n - 1;
+        };
+        const size_t n = static_cast<size_t>(n_);
+        std::vector<uint8_t> chosen(n, 0);
+        std::vector<double> sims(n), cum(n);
+        std::vector<int64_t> ptr(n + 1);
+        CK(cudaMemcpyAsync(ptr.data(), indptr_.p, (n + 1) * 8, cudaMemcpyDeviceToHost, stream_));
+        DevBuf<float> dense;
+        dense.alloc(d_);
+        CK(cudaMemsetAsync(dense.p, 0, d_ * sizeof(float), stream_));
+        launch(fill_u32_kernel, grid_for(n_, 256), 256, a_.p, n_, 0);
+        launch(fill_f64_kernel, grid_for(n_, 256), 256, sims_.p, n_, -2.0);
+        CK_LAUNCH();
+        std::vector<uint32_t> seeds;
+        auto add_seed = [&](size_t doc, uint32_t cluster) {
+            chosen[doc] = 1;
+            seeds.push_back(static_cast<uint32_t>(doc));
+            launch(scatter_row_kernel, 1, 256, indptr_.p, idx_.p, val_.p, doc, dense.p, 0);
+            launch(kpp_round_kernel, grid_for(n_ * 32, 256), 256, indptr_.p, idx_.p, val_.p, n_,
+                                                                          dense.p, cluster, a_.p, sims_.p);
+            launch(scatter_row_kernel, 1, 256, indptr_.p, idx_.p, val_.p, doc, dense.p, 1);
+            CK_LAUNCH();
+        };
+        add_seed(uniform_index(n), 0);
+        for (uint32_t c = 1; c < k_; ++c) {
+            CK(cudaMemcpyAsync(sims.data(), sims_.p, n * 8, cudaMemcpyDeviceToHost, stream_));
+            CK(cudaStreamSynchronize(stream_));
+            double total = 0.0;
+            for (size_t i = 0; i < n; ++i) {
+                double w = 0.0;
+                if (!chosen[i]) {
+                    const double dd = 1.0 - sims[i];
+                    if (dd > 0.0) w = dd * dd;
+                }
+                total += w;
+                cum[i] = total;
+            }
+            size_t pick;
+            if (total > 0.0) {
+                const double target = uniform_unit() * total;
+                pick = static_cast<size_t>(std::upper_bound(cum.begin(), cum.end(), target) - cum.begin());
+                if (pick >= n) {
+                    pick = n - 1;
+                    while (chosen[pick]) --pick;
+                }
+            } else {
+                pick = 0;
+                while (chosen[pick]) ++pick;
+            }
+            add_seed(pick, c);
+        }
+        // Cᵀ = the seed documents (informational; the first update recomputes all)
+        DevBuf<uint32_t> dseeds;
+        dseeds.alloc(k_);
+        CK(cudaMemcpyAsync(dseeds.p, seeds.data(), k_ * 4, cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemsetAsync(ct_.p, 0, static_cast<uint64_t>(d_) * ld_ * sizeof(float), stream_));
+        launch(scatter_seeds_kernel, grid_for(static_cast<int64_t>(k_) * 32, 256), 256, 
+            indptr_.p, idx_.p, val_.p, dseeds.p, k_, ct_.p, ld_);
+        CK_LAUNCH();
+        reset_sums();
+        CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
+        iteration_ = 0;
+        have_cc_ = false;
+        state_ = true;
+        CK(cudaStreamSynchronize(stream_));
+        if (seeds_out) std::memcpy(seeds_out, seeds.data(), k_ * 4);
+    }
+
+    // ------------------------------------------------------------ update --
+    // compute_centroids + detect_unchanged for a single context (1 GPU).
+    void update(sskm_iteration_stats* st) {
+        need_state();
+        CK(cudaEventRecord(ev_[0], stream_));
+        iteration_ += 1;
+        repaired_.clear();
+        local_counts_device();
+        repair_empty_single();
+        // rows that moved since the sums were last brought up to date
+        reset_scalars();
+        launch(moved_kernel, grid_for(n_, 256), 256, a_.p, a_sum_.p, n_, moved_.p, &scal_.p->n_moved);
+        CK_LAUNCH();
+        launch(delta_local_kernel, grid_for(n_ * 32, 256), 256, 
+            indptr_.p, idx_.p, val_.p, moved_.p, &scal_.p->n_moved, a_.p, a_sum_.p, S_.p, ld_, K_,
+            touched_.p);
+        CK_LAUNCH();
+        finish_update(st);
+        CK(cudaEventRecord(ev_[1], stream_));
+        CK(cudaEventSynchronize(ev_[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        st->update_ms = ms;
+    }
+
+    // Multi-GPU update: apply rows gathered from every rank, then finish.
+    void update_apply(int64_t n_moved, const uint32_t* old_c, const uint32_t* new_c, const int64_t* row_ptr,
+                      const int32_t* idx, const float* val, const uint32_t* repaired, uint32_t n_repaired,
+                      sskm_iteration_stats* st) {
+        need_state();
+        CK(cudaEventRecord(ev_[0], stream_));
+        iteration_ += 1;
+        repaired_.assign(repaired, repaired + n_repaired);
+        CK(cudaMemsetAsync(repaired_flag_.p, 0, k_, stream_));
+        if (!repaired_.empty()) {
+            std::vector<uint8_t> f(k_, 0);
+            for (uint32_t j : repaired_) f[j] = 1;
+            CK(cudaMemcpyAsync(repaired_flag_.p, f.data(), k_, cudaMemcpyHostToDevice, stream_));
+        }
+        // local owner map catches up (the local rows are part of the gathered set)
+        fill_sum_owner_local();
+        reset_scalars();
+        if (n_moved > 0) {
+            launch(delta_packed_kernel, grid_for(n_moved * 32, 256), 256, 
+                n_moved, old_c, new_c, row_ptr, idx, val, S_.p, ld_, K_, touched_.p);
+            CK_LAUNCH();
+        }
+        finish_update(st);
+        CK(cudaEventRecord(ev_[1], stream_));
+        CK(cudaEventSynchronize(ev_[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        st->update_ms = ms;
+        st->n_moved = static_cast<uint64_t>(n_moved);
+    }
+
+    // ------------------------------------------------------------ assign --
+    void assign(sskm_iteration_stats* st) {
+        need_state();
+        const bool full = iteration_ <= 1 || cfg_.mode == SSKM_MODE_BASELINE;
+        st->iteration = iteration_;
+        if (full) {
+            full_assign(st);
+        } else {
+            ncc_assign(st);
+        }
+        st->index_active = 0;
+    }
+
+    void full_assign(sskm_iteration_stats* st) {
+        CK(cudaEventRecord(ev_[2], stream_));
+        CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+        AssignArgs p = base_args();
+        p.M = ct_.p;
+        p.ld = ld_;
+        p.ncols = k_;
+        p.col_ids = nullptr;
+        p.doc_list = nullptr;
+        p.n_work = n_;
+        CK(cudaEventRecord(ev_[4], stream_));
+        launch_scan<kInitFull>(p, k_);
+        CK(cudaEventRecord(ev_[5], stream_));
+        finish_assign(st);
+        st->n_unchanged_centroids = iteration_ <= 1 ? 0 : n_unchanged_;
+        st->dot_products = static_cast<uint64_t>(k_) * static_cast<uint64_t>(n_);
+        st->gpu_dot_products = st->dot_products;
+        st->n_changed = k_;
+        st->n_rescan = 0;
+        timing(st);
+    }
+
+    void ncc_assign(sskm_iteration_stats* st) {
+        CK(cudaEventRecord(ev_[2], stream_));
+        CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+        ensure_cc();
+        reset_scalars();
+        AssignArgs p = base_args();
+        p.M = cc_.p;
+        p.ld = ld_cc_;
+        p.ncols = n_chg_;
+        p.col_ids = chg_ids_.p;
+        p.doc_list = nullptr;
+        p.n_work = n_;
+        CK(cudaEventRecord(ev_[4], stream_));
+        launch_scan<kInitNcc>(p, n_chg_);
+        pull_scalars();
+        const uint64_t n_rescan = hs_->n_rescan;
+        if (n_rescan > 0) {
+            AssignArgs q = base_args();
+            q.M = ct_.p;
+            q.ld = ld_;
+            q.ncols = k_;
+            q.col_ids = nullptr;
+            q.doc_list = rescan_.p;
+            q.n_work = static_cast<int64_t>(n_rescan);
+            launch_scan<kInitRescan>(q, k_);
+        }
+        CK(cudaEventRecord(ev_[5], stream_));
+        finish_assign(st);
+        // dot accounting of the reference (engine.cpp:253-306): every document
+        // evaluates the changed list (minus its own centroid, which a
+        // changed-own document evaluates as its refresh), plus the unchanged
+        // list when the refreshed scan did not beat the cache.
+        const uint64_t n_unch = k_ - n_chg_;
+        st->n_unchanged_centroids = static_cast<uint32_t>(n_unch);
+        st->dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_rescan * n_unch;
+        st->gpu_dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_rescan * k_;
+        st->n_changed = n_chg_;
+        st->n_rescan = n_rescan;
+        timing(st);
+    }
+
+    // ------------------------------------------------------------ access --
+    void get_state(uint32_t* a, double* sims, uint8_t* unchanged) {
+        need_state();
+        if (a) CK(cudaMemcpyAsync(a, a_.p, n_ * 4, cudaMemcpyDeviceToHost, stream_));
+        if (sims) CK(cudaMemcpyAsync(sims, sims_.p, n_ * 8, cudaMemcpyDeviceToHost, stream_));
+        if (unchanged) CK(cudaMemcpyAsync(unchanged, unchanged_.p, k_, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void set_state(const uint32_t* a, const double* sims, uint32_t iteration) {
+        need_config();
+        if (!state_) {
+            reset_sums();
+            CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
+            CK(cudaMemsetAsync(ct_.p, 0, static_cast<uint64_t>(d_) * ld_ * 4, stream_));
+            state_ = true;
+        }
+        if (a) {
+            for (int64_t i = 0; i < n_; ++i)
+                if (a[i] >= k_) throw InvalidArgument("assignment out of range");
+            CK(cudaMemcpyAsync(a_.p, a, n_ * 4, cudaMemcpyHostToDevice, stream_));
+        }
+        if (sims) CK(cudaMemcpyAsync(sims_.p, sims, n_ * 8, cudaMemcpyHostToDevice, stream_));
+        iteration_ = iteration;
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void get_centroids(float* ct) {
+        need_state();
+        CK(cudaMemcpy2DAsync(ct, k_ * sizeof(float), ct_.p, ld_ * sizeof(float), k_ * sizeof(float), d_,
+                             cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    // Teacher forcing: replaces Cᵀ; the sums no longer describe it, so they are
+    // rebuilt from scratch by the next update.
+    void set_centroids(const float* ct) {
+        need_config();
+        if (!state_) set_state(nullptr, nullptr, iteration_);
+        CK(cudaMemsetAsync(ct_.p, 0, static_cast<uint64_t>(d_) * ld_ * 4, stream_));
+        CK(cudaMemcpy2DAsync(ct_.p, ld_ * sizeof(float), ct, k_ * sizeof(float), k_ * sizeof(float), d_,
+                             cudaMemcpyHostToDevice, stream_));
+        reset_sums();
+        have_cc_ = false;
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void set_unchanged(const uint8_t* flags) {
+        need_state();
+        CK(cudaMemcpyAsync(unchanged_.p, flags, k_, cudaMemcpyHostToDevice, stream_));
+        have_cc_ = false;
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    const std::vector<uint32_t>& repaired() const { return repaired_; }
+    uint32_t iteration() const { return iteration_; }
+    uint32_t k() const { return k_; }
+    int64_t n() const { return n_; }
+    uint32_t d() const { return d_; }
+    const sskm_run_config& config() const { return cfg_; }
+
+    // -------------------------------------------------- multi-GPU pieces --
+    void local_counts(int64_t* out) {
+        need_state();
+        local_counts_device();
+        CK(cudaMemcpyAsync(out, counts_.p, k_ * 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void local_donor(const int64_t* global_counts, double* sim, int64_t* doc) {
+        need_state();
+        CK(cudaMemcpyAsync(counts_.p, global_counts, k_ * 8, cudaMemcpyHostToDevice, stream_));
+        uint64_t idx = find_donor();
+        if (idx == ULLONG_MAX) {
+            *doc = INT64_MAX;
+            *sim = 0.0;
+            return;
+        }
+        double s;
+        CK(cudaMemcpyAsync(&s, sims_.p + idx, 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        *sim = s;
+        *doc = static_cast<int64_t>(idx) + doc_offset_;
+    }
+
+    void move_doc(int64_t global_doc, uint32_t cluster) {
+        need_state();
+        const int64_t i = global_doc - doc_offset_;
+        if (i < 0 || i >= n_ || cluster >= k_) throw InvalidArgument("move_doc out of range");
+        CK(cudaMemcpyAsync(a_.p + i, &cluster, 4, cudaMemcpyHostToDevice, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void moved_size(int64_t* n_moved, int64_t* nnz_moved) {
+        need_state();
+        reset_scalars();
+        launch(moved_kernel, grid_for(n_, 256), 256, a_.p, a_sum_.p, n_, moved_.p, &scal_.p->n_moved);
+        CK_LAUNCH();
+        pull_scalars();
+        const uint64_t m = hs_->n_moved;
+        moved_host_.resize(m);
+        if (m) CK(cudaMemcpyAsync(moved_host_.data(), moved_.p, m * 4, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        std::sort(moved_host_.begin(), moved_host_.end());
+        ptr_host_.resize(n_ + 1);
+        CK(cudaMemcpy(ptr_host_.data(), indptr_.p, (n_ + 1) * 8, cudaMemcpyDeviceToHost));
+        int64_t nnz = 0;
+        for (uint32_t i : moved_host_) nnz += ptr_host_[i + 1] - ptr_host_[i];
+        *n_moved = static_cast<int64_t>(m);
+        *nnz_moved = nnz;
+    }
+
+    // Host-side packing of the local moved rows (ascending local doc order).
+    void moved_pack(int64_t* doc_ids, uint32_t* old_c, uint32_t* new_c, int64_t* row_ptr, int32_t* idx,
+                    float* val) {
+        need_state();
+        std::vector<uint32_t> a(n_), as(n_);
+        CK(cudaMemcpy(a.data(), a_.p, n_ * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(as.data(), a_sum_.p, n_ * 4, cudaMemcpyDeviceToHost));
+        int64_t p = 0;
+        row_ptr[0] = 0;
+        for (size_t m = 0; m < moved_host_.size(); ++m) {
+            const uint32_t i = moved_host_[m];
+            doc_ids[m] = static_cast<int64_t>(i) + doc_offset_;
+            old_c[m] = as[i];
+            new_c[m] = a[i];
+            const int64_t b = ptr_host_[i], e = ptr_host_[i + 1];
+            if (e > b) {
+                CK(cudaMemcpy(idx + p, idx_.p + b, (e - b) * 4, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(val + p, val_.p + b, (e - b) * 4, cudaMemcpyDeviceToHost));
+            }
+            p += e - b;
+            row_ptr[m + 1] = p;
+        }
+    }
+
+    double local_sims_sum() {
+        need_state();
+        launch(local_sum_kernel, kObjBlocks, 256, sims_.p, n_, obj_part_.p);
+        launch(sum_parts_kernel, 1, 32, obj_part_.p, kObjBlocks, &scal_.p->objective);
+        CK_LAUNCH();
+        pull_scalars();
+        return hs_->objective;
+    }
+
+private:
+    static constexpr int kObjBlocks = 512;
+
+    void need_config() const {
+        if (!corpus_) throw InvalidArgument("no corpus uploaded");
+        if (k_ == 0) throw InvalidArgument("context not configured");
+    }
+    void need_state() const {
+        need_config();
+        if (!state_) throw InvalidArgument("no clustering state: initialise from seeds or k-means++ first");
+    }
+
+    unsigned grid_for(int64_t threads, int block) const {
+        const int64_t b = (threads + block - 1) / block;
+        const int64_t cap = static_cast<int64_t>(sms_) * 32;
+        return static_cast<unsigned>(std::max<int64_t>(1, std::min(b, cap)));
+    }
+
+    void reset_scalars() {
+        CK(cudaMemsetAsync(scal_.p, 0, sizeof(Scalars), stream_));
+    }
+    void pull_scalars() {
+        CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void seed_assign_state() {
+        launch(fill_u32_kernel, grid_for(n_, 256), 256, a_.p, n_, 0);
+        launch(fill_f64_kernel, grid_for(n_, 256), 256, sims_.p, n_, -2.0);
+        CK_LAUNCH();
+        reset_sums();
+        CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
+        iteration_ = 0;
+        have_cc_ = false;
+        state_ = true;
+    }
+
+    void fill_sum_owner_local() {
+        // after a multi-GPU exchange the local rows are summed under their new cluster
+        CK(cudaMemcpyAsync(a_sum_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+    }
+
+    void local_counts_device() {
+        CK(cudaMemsetAsync(counts_.p, 0, k_ * 8, stream_));
+        reset_scalars();
+        launch(counts_kernel, grid_for(n_, 256), 256, a_.p, n_, k_, counts_.p, &scal_.p->bad);
+        CK_LAUNCH();
+    }
+
+    uint64_t find_donor() {
+        // requires counts_ to hold the (global) cluster sizes
+        CK(cudaMemsetAsync(&scal_.p->donor_key, 0xFF, 8, stream_));
+        CK(cudaMemsetAsync(&scal_.p->donor_idx, 0xFF, 8, stream_));
+        launch(donor_sim_kernel, grid_for(n_, 256), 256, a_.p, sims_.p, n_, counts_.p,
+                                                                 &scal_.p->donor_key);
+        launch(donor_idx_kernel, grid_for(n_, 256), 256, a_.p, sims_.p, n_, counts_.p,
+                                                                 &scal_.p->donor_key, &scal_.p->donor_idx);
+        CK_LAUNCH();
+        pull_scalars();
+        return hs_->donor_idx;
+    }
+
+    // Empty-cluster repair for one context (engine.cpp:154-167): ascending
+    // empty clusters, each taking the lowest-(sim, index) document from a
+    // cluster that can spare it. Rare path; host-sequenced small kernels.
+    void repair_empty_single() {
+        launch(count_empty_kernel, grid_for(k_, 256), 256, counts_.p, k_, &scal_.p->n_empty);
+        CK_LAUNCH();
+        pull_scalars();
+        if (hs_->bad) throw InvalidArgument("assignment out of range");
+        CK(cudaMemsetAsync(repaired_flag_.p, 0, k_, stream_));
+        if (hs_->n_empty == 0) return;
+        std::vector<unsigned long long> counts(k_);
+        CK(cudaMemcpyAsync(counts.data(), counts_.p, k_ * 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        std::vector<uint8_t> flag(k_, 0);
+        for (uint32_t j = 0; j < k_; ++j) {
+            if (counts[j] != 0) continue;
+            const uint64_t donor = find_donor();
+            if (donor == ULLONG_MAX) throw CudaError("empty-cluster repair found no donor");
+            uint32_t old_c;
+            CK(cudaMemcpyAsync(&old_c, a_.p + donor, 4, cudaMemcpyDeviceToHost, stream_));
+            CK(cudaStreamSynchronize(stream_));
+            --counts[old_c];
+            counts[j] = 1;
+            CK(cudaMemcpyAsync(a_.p + donor, &j, 4, cudaMemcpyHostToDevice, stream_));
+            CK(cudaMemcpyAsync(counts_.p + old_c, &counts[old_c], 8, cudaMemcpyHostToDevice, stream_));
+            CK(cudaMemcpyAsync(counts_.p + j, &counts[j], 8, cudaMemcpyHostToDevice, stream_));
+            CK(cudaStreamSynchronize(stream_));
+            repaired_.push_back(j);
+            flag[j] = 1;
+        }
+        CK(cudaMemcpyAsync(repaired_flag_.p, flag.data(), k_, cudaMemcpyHostToDevice, stream_));
+    }
+
+    // Renormalise touched columns, drift, unchanged flags, changed list.
+    void finish_update(sskm_iteration_stats* st) {
+        // touched clusters, ascending
+        launch(compact_ids_kernel, 1, 1024, touched_.p, k_, 1, rec_ids_.p, &scal_.p->n_rec);
+        CK_LAUNCH();
+        pull_scalars();
+        const uint32_t n_rec = hs_->n_rec;
+        const uint32_t n_rb = static_cast<uint32_t>(ceil_div(d_, kRowBlock));
+        if (n_rec > 0) {
+            dim3 grid(static_cast<unsigned>(ceil_div(n_rec, 128)), n_rb);
+            launch(norm2_partial_kernel, grid, 128, S_.p, ld_, d_, rec_ids_.p, n_rec, part_.p);
+            launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(n_rec, 128)), 128, 
+                part_.p, n_rb, n_rec, norm2_.p);
+            launch(write_cols_kernel, grid, 128, S_.p, ct_.p, ld_, d_, rec_ids_.p, n_rec, norm2_.p,
+                                                         part_.p, &scal_.p->zero_flag);
+            launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(n_rec, 128)), 128, 
+                part_.p, n_rb, n_rec, drift_rec_.p);
+            launch(scatter_pos_kernel, grid_for(n_rec, 256), 256, rec_ids_.p, n_rec, rec_pos_.p);
+            CK_LAUNCH();
+        }
+        launch(flags_kernel, grid_for(k_, 256), 256, 
+            k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon, touched_.p, repaired_flag_.p, rec_pos_.p,
+            drift_rec_.p, unchanged_.p, drift_.p, &scal_.p->max_drift_bits, &scal_.p->n_unchanged);
+        CK_LAUNCH();
+        CK(cudaMemsetAsync(touched_.p, 0, k_, stream_));
+        pull_scalars();
+        if (hs_->zero_flag) throw InvalidArgument("cannot normalize zero vector");
+        n_unchanged_ = hs_->n_unchanged;
+        double max_drift;
+        std::memcpy(&max_drift, &hs_->max_drift_bits, 8);
+        have_cc_ = false;
+        std::memset(st, 0, sizeof(*st));
+        st->iteration = iteration_;
+        st->n_unchanged_centroids = n_unchanged_;
+        st->max_sq_drift = iteration_ <= 1 ? 0.0 : max_drift;
+        st->n_repaired = static_cast<int32_t>(repaired_.size());
+        st->n_moved = hs_->n_moved;
+        st->n_recomputed = n_rec;
+    }
+
+    void ensure_cc() {
+        if (have_cc_) return;
+        launch(compact_ids_kernel, 1, 1024, unchanged_.p, k_, 0, chg_ids_.p, &scal_.p->n_chg);
+        CK_LAUNCH();
+        pull_scalars();
+        n_chg_ = hs_->n_chg;
+        ld_cc_ = std::max<uint64_t>(128, round_up(n_chg_, 128));
+        if (n_chg_ > 0) {
+            cc_.alloc(static_cast<uint64_t>(d_) * ld_);
+            launch(gather_cols_kernel, grid_for(static_cast<int64_t>(d_) * ld_cc_, 256), 256, 
+                ct_.p, ld_, d_, chg_ids_.p, n_chg_, cc_.p, ld_cc_);
+            CK_LAUNCH();
+        }
+        have_cc_ = true;
+    }
+
+    AssignArgs base_args() const {
+        AssignArgs p{};
+        p.indptr = indptr_.p;
+        p.idx = idx_.p;
+        p.val = val_.p;
+        p.CT = ct_.p;
+        p.ld_ct = ld_;
+        p.unchanged = unchanged_.p;
+        p.a = a_.p;
+        p.sims = sims_.p;
+        p.rescan_list = rescan_.p;
+        p.n_rescan = &scal_.p->n_rescan;
+        return p;
+    }
+
+    template <int INIT>
+    void launch_scan(const AssignArgs& p, uint32_t ncols) {
+        const unsigned grid = grid_for(p.n_work * 32, 256);
+        if (ncols > 64 || INIT == kInitFull || INIT == kInitRescan) {
+            launch(assign_kernel<4, INIT>, grid, 256, p);
+        } else if (ncols > 32) {
+            launch(assign_kernel<2, INIT>, grid, 256, p);
+        } else {
+            launch(assign_kernel<1, INIT>, grid, 256, p);
+        }
+        CK_LAUNCH();
+    }
+
+    void finish_assign(sskm_iteration_stats* st) {
+        reset_scalars_keep_rescan();
+        launch(finish_assign_kernel, kObjBlocks, 256, a_.p, a_start_.p, sims_.p, n_, obj_part_.p,
+                                                              &scal_.p->reassigned);
+        launch(sum_parts_kernel, 1, 32, obj_part_.p, kObjBlocks, &scal_.p->objective);
+        CK_LAUNCH();
+        CK(cudaEventRecord(ev_[3], stream_));
+        pull_scalars();
+        st->n_reassigned = hs_->reassigned;
+        st->objective = hs_->objective;
+    }
+
+    void reset_scalars_keep_rescan() {
+        CK(cudaMemsetAsync(&scal_.p->reassigned, 0, 8, stream_));
+        CK(cudaMemsetAsync(&scal_.p->objective, 0, 8, stream_));
+    }
+
+    void timing(sskm_iteration_stats* st) {
+        float ms = 0.f, kms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+        CK(cudaEventElapsedTime(&kms, ev_[4], ev_[5]));
+        st->assign_ms = ms;
+        st->assign_kernel_ms = kms;
+    }
+
+    int device_;
+    int sms_ = 148;
+    cudaStream_t stream_{};
+    cudaEvent_t ev_[8]{};
+    static constexpr int kUserEvents = 16;
+    cudaEvent_t user_ev_[kUserEvents]{};
+    uint64_t launches_ = 0;
+    DevBuf<Scalars> scal_;
+    Scalars* hs_ = nullptr;
+
+    bool corpus_ = false, state_ = false, have_cc_ = false;
+    int64_t n_ = 0, n_total_ = 0, doc_offset_ = 0, nnz_ = 0;
+    uint32_t d_ = 0, k_ = 0, ld_ = 0;
+    int K_ = 0;
+    uint32_t iteration_ = 0, n_unchanged_ = 0, n_chg_ = 0;
+    uint64_t ld_cc_ = 128;
+    sskm_run_config cfg_{};
+    std::vector<double> lambdas_;
+    std::vector<uint32_t> repaired_;
+    std::vector<uint32_t> moved_host_;
+    std::vector<int64_t> ptr_host_;
+
+    DevBuf<int64_t> indptr_;
+    DevBuf<int32_t> idx_;
+    DevBuf<float> val_;
+    DevBuf<float> ct_, cc_;
+    DevBuf<long long> S_;
+    DevBuf<uint32_t> a_, a_sum_, a_start_, moved_, rescan_, rec_ids_, rec_pos_, chg_ids_;
+    DevBuf<double> sims_, drift_, norm2_, drift_rec_, part_, obj_part_;
+    DevBuf<uint8_t> unchanged_, touched_, repaired_flag_;
+    DevBuf<unsigned long long> counts_;
+};
+
+}  // namespace sskm_b200
+
+// ====================================================================== C-ABI
+using sskm_b200::Engine;
+
+struct sskm_ctx {
+    std::unique_ptr<Engine> eng;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return SSKM_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SSKM_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SSKM_ERUNTIME;
+    } catch (...) {
+        g_err = "unknown error";
+        return SSKM_ERUNTIME;
+    }
+}
+
+Engine& E(sskm_ctx* c) {
+    if (!c || !c->eng) throw sskm_b200::InvalidArgument("null context");
+    return *c->eng;
+}
+
+bool stop_after(const sskm_iteration_stats& st, double conv, int32_t* reason) {
+    if (st.n_reassigned == 0) {
+        *reason = SSKM_STOP_NO_REASSIGNMENTS;
+        return true;
+    }
+    if (st.iteration > 1 && st.max_sq_drift < conv) {
+        *reason = SSKM_STOP_CENTROID_DRIFT;
+        return true;
+    }
+    return false;
+}
+
+void step(Engine& e, sskm_iteration_stats* st) {
+    const auto t0 = std::chrono::steady_clock::now();
+    e.update(st);
+    sskm_iteration_stats a{};
+    e.assign(&a);
+    st->n_reassigned = a.n_reassigned;
+    st->dot_products = a.dot_products;
+    st->gpu_dot_products = a.gpu_dot_products;
+    st->n_changed = a.n_changed;
+    st->n_rescan = a.n_rescan;
+    st->objective = a.objective;
+    st->assign_ms = a.assign_ms;
+    st->assign_kernel_ms = a.assign_kernel_ms;
+    st->index_active = 0;
+    st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+extern "C" {
+
+const char* sskm_last_error(void) { return g_err.c_str(); }
+
+int sskm_validate(const sskm_run_config* cfg, uint64_t n_docs) {
+    return guard([&] {
+        if (!cfg) throw sskm_b200::InvalidArgument("null config");
+        Engine::validate(*cfg, n_docs);
+    });
+}
+
+int sskm_open(int32_t device, sskm_ctx** out) {
+    return guard([&] {
+        if (!out) throw sskm_b200::InvalidArgument("null output");
+        auto* c = new sskm_ctx();
+        try {
+            c->eng = std::make_unique<Engine>(device);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int sskm_close(sskm_ctx* ctx) {
+    return guard([&] { delete ctx; });
+}
+
+int sskm_upload_csr(sskm_ctx* ctx, int64_t n_docs, uint32_t dims, const int64_t* indptr,
+                    const int32_t* indices, const float* values, int64_t doc_offset, int64_t n_docs_total) {
+    return guard([&] { E(ctx).upload(n_docs, dims, indptr, indices, values, doc_offset, n_docs_total); });
+}
+
+int sskm_configure(sskm_ctx* ctx, const sskm_run_config* cfg) {
+    return guard([&] {
+        if (!cfg) throw sskm_b200::InvalidArgument("null config");
+        E(ctx).configure(*cfg);
+    });
+}
+
+int sskm_init_from_seeds(sskm_ctx* ctx, const uint32_t* seeds) {
+    return guard([&] { E(ctx).init_from_seeds(seeds); });
+}
+
+int sskm_init_kmeanspp(sskm_ctx* ctx, uint64_t seed, uint32_t* seeds_out) {
+    return guard([&] { E(ctx).init_kmeanspp(seed, seeds_out); });
+}
+
+int sskm_update(sskm_ctx* ctx, sskm_iteration_stats* st) {
+    return guard([&] { E(ctx).update(st); });
+}
+
+int sskm_assign(sskm_ctx* ctx, sskm_iteration_stats* st) {
+    return guard([&] {
+        std::memset(st, 0, sizeof(*st));
+        E(ctx).assign(st);
+    });
+}
+
+int sskm_step(sskm_ctx* ctx, sskm_iteration_stats* st) {
+    return guard([&] { step(E(ctx), st); });
+}
+
+int sskm_run(sskm_ctx* ctx, sskm_iteration_stats* stats, uint32_t cap, uint32_t* n_iters, int32_t* stop_reason) {
+    return guard([&] {
+        Engine& e = E(ctx);
+        int32_t reason = SSKM_STOP_MAX_ITERATIONS;
+        uint32_t t = 0;
+        for (uint32_t iter = 1; iter <= e.config().max_iters; ++iter) {
+            sskm_iteration_stats st{};
+            step(e, &st);
+            if (stats && t < cap) stats[t] = st;
+            ++t;
+            if (stop_after(st, e.config().conv_sq_dist, &reason)) break;
+        }
+        if (n_iters) *n_iters = t;
+        if (stop_reason) *stop_reason = reason;
+    });
+}
+
+int sskm_get_state(sskm_ctx* ctx, uint32_t* a, double* sims, uint8_t* unchanged) {
+    return guard([&] { E(ctx).get_state(a, sims, unchanged); });
+}
+
+int sskm_set_state(sskm_ctx* ctx, const uint32_t* a, const double* sims, uint32_t iteration) {
+    return guard([&] { E(ctx).set_state(a, sims, iteration); });
+}
+
+int sskm_set_unchanged(sskm_ctx* ctx, const uint8_t* flags) {
+    return guard([&] { E(ctx).set_unchanged(flags); });
+}
+
+int sskm_get_centroids(sskm_ctx* ctx, float* ct) {
+    return guard([&] { E(ctx).get_centroids(ct); });
+}
+
+int sskm_set_centroids(sskm_ctx* ctx, const float* ct) {
+    return guard([&] { E(ctx).set_centroids(ct); });
+}
+
+int sskm_get_repaired(sskm_ctx* ctx, uint32_t* repaired, uint32_t* n_repaired) {
+    return guard([&] {
+        const auto& r = E(ctx).repaired();
+        if (repaired) std::memcpy(repaired, r.data(), r.size() * 4);
+        *n_repaired = static_cast<uint32_t>(r.size());
+    });
+}
+
+int sskm_get_iteration(sskm_ctx* ctx, uint32_t* iteration) {
+    return guard([&] { *iteration = E(ctx).iteration(); });
+}
+
+int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims, const int64_t* indptr,
+                     const int32_t* indices, const float* values, const uint32_t* seeds, uint32_t* assignments,
+                     double* sims, float* ct, sskm_iteration_stats* stats, uint32_t stats_cap,
+                     uint32_t* n_iters, int32_t* stop_reason, double* objective) {
+    return guard([&] {
+        if (!cfg) throw sskm_b200::InvalidArgument("null config");
+        Engine::validate(*cfg, n_docs > 0 ? static_cast<uint64_t>(n_docs) : 0);
+        Engine e(cfg->device);
+        e.upload(n_docs, dims, indptr, indices, values, 0, n_docs);
+        e.configure(*cfg);
+        if (seeds) {
+            e.init_from_seeds(seeds);
+        } else {
+            e.init_kmeanspp(cfg->seed, nullptr);
+        }
+        int32_t reason = SSKM_STOP_MAX_ITERATIONS;
+        uint32_t t = 0;
+        double obj = 0.0;
+        for (uint32_t iter = 1; iter <= cfg->max_iters; ++iter) {
+            sskm_iteration_stats st{};
+            step(e, &st);
+            if (stats && t < stats_cap) stats[t] = st;
+            ++t;
+            obj = st.objective;
+            if (stop_after(st, cfg->conv_sq_dist, &reason)) break;
+        }
+        e.get_state(assignments, sims, nullptr);
+        if (ct) e.get_centroids(ct);
+        if (n_iters) *n_iters = t;
+        if (stop_reason) *stop_reason = reason;
+        if (objective) *objective = obj;
+    });
+}
+
+int sskm_local_counts(sskm_ctx* ctx, int64_t* counts) {
+    return guard([&] { E(ctx).local_counts(counts); });
+}
+
+int sskm_local_donor(sskm_ctx* ctx, const int64_t* global_counts, double* sim, int64_t* doc) {
+    return guard([&] { E(ctx).local_donor(global_counts, sim, doc); });
+}
+
+int sskm_move_doc(sskm_ctx* ctx, int64_t global_doc, uint32_t cluster) {
+    return guard([&] { E(ctx).move_doc(global_doc, cluster); });
+}
+
+int sskm_moved_size(sskm_ctx* ctx, int64_t* n_moved, int64_t* nnz_moved) {
+    return guard([&] { E(ctx).moved_size(n_moved, nnz_moved); });
+}
+
+int sskm_moved_pack(sskm_ctx* ctx, int64_t* doc_ids, uint32_t* old_c, uint32_t* new_c, int64_t* row_ptr,
+                    int32_t* idx, float* val) {
+    return guard([&] { E(ctx).moved_pack(doc_ids, old_c, new_c, row_ptr, idx, val); });
+}
+
+int sskm_update_apply(sskm_ctx* ctx, int64_t n_moved, const uint32_t* old_c, const uint32_t* new_c,
+                      const int64_t* row_ptr, const int32_t* idx, const float* val, const uint32_t* repaired,
+                      uint32_t n_repaired, sskm_iteration_stats* st) {
+    return guard([&] { E(ctx).update_apply(n_moved, old_c, new_c, row_ptr, idx, val, repaired, n_repaired, st); });
+}
+
+int sskm_timer_record(sskm_ctx* ctx, int32_t slot) {
+    return guard([&] { E(ctx).timer_record(slot); });
+}
+
+int sskm_timer_elapsed(sskm_ctx* ctx, int32_t a, int32_t b, double* ms) {
+    return guard([&] { *ms = E(ctx).timer_elapsed(a, b); });
+}
+
+int sskm_launch_count(sskm_ctx* ctx, uint64_t* n) {
+    return guard([&] { *n = E(ctx).launches(); });
+}
+
+int sskm_synchronize(sskm_ctx* ctx) {
+    return guard([&] { E(ctx).synchronize(); });
+}
+
+int sskm_local_sims_sum(sskm_ctx* ctx, double* sum) {
+    return guard([&] { *sum = E(ctx).local_sims_sum(); });
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// Centroid-update kernels (replace compute_centroids, engine.cpp:137-195,
+// DenseAccumulator, sparse_vector.cpp:237-274, normalize, :160-209, and
+// detect_unchanged / sq_euclidean, engine.cpp:197-216, sparse_vector.cpp:211-235).
+//
+// Cluster sums are kept resident in HBM as exact fixed-point integers
+// S[t][j] = Σ_{i∈j} round(x_it · 2^K) (int64, term-major like Cᵀ). Integer
+// addition is associative, so the sums are bitwise independent of document
+// order, thread schedule and GPU count, and an iteration only has to apply the
+// rows of documents that MOVED (S_new = S_old + Σ_in − Σ_out exactly). K is
+// chosen so that N·2^K < 2^62 for unit rows (|x| ≤ 1): no overflow is
+// possible. Only the columns of clusters whose membership changed are then
+// renormalised (fp64) and rewritten; a cluster with unchanged membership keeps
+// a bitwise-identical column, which is exactly the reference's ncc_epsilon = 0
+// "unchanged" condition.
+#pragma once
+
+#include "common.cuh"
+
+namespace sskm_b200 {
+
+__global__ void counts_kernel(const uint32_t* __restrict__ a, int64_t n, uint32_t k,
+                              unsigned long long* __restrict__ counts, unsigned int* bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t c = a[i];
+        if (c >= k) {
+            atomicOr(bad, 1u);
+            continue;
+        }
+        atomicAdd(counts + c, 1ull);
+    }
+}
+
+__global__ void count_empty_kernel(const unsigned long long* __restrict__ counts, uint32_t k,
+                                   unsigned int* n_empty) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+        if (counts[j] == 0) atomicAdd(n_empty, 1u);
+}
+
+// Donor for empty-cluster repair (engine.cpp:156-161): lowest cached sim among
+// documents in clusters of size >= 2, ties to the lowest document index. Two
+// order-independent atomicMin passes give the reference's sequential answer.
+__global__ void donor_sim_kernel(const uint32_t* __restrict__ a, const double* __restrict__ sims,
+                                 int64_t n, const unsigned long long* __restrict__ counts,
+                                 unsigned long long* key) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (counts[a[i]] < 2) continue;
+        atomicMin(key, orderable(sims[i]));
+    }
+}
+
+__global__ void donor_idx_kernel(const uint32_t* __restrict__ a, const double* __restrict__ sims,
+                                 int64_t n, const unsigned long long* __restrict__ counts,
+                                 const unsigned long long* key, unsigned long long* idx_out) {
+    const unsigned long long kk = *key;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (counts[a[i]] < 2) continue;
+        if (orderable(sims[i]) == kk) atomicMin(idx_out, static_cast<unsigned long long>(i));
+    }
+}
+
+// Documents whose cluster differs from the cluster their row is summed into.
+__global__ void moved_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_sum,
+                             int64_t n, uint32_t* __restrict__ moved,
+                             unsigned long long* n_moved) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (a[i] != a_sum[i]) {
+            const unsigned long long pos = atomicAdd(n_moved, 1ull);
+            moved[pos] = static_cast<uint32_t>(i);
+        }
+    }
+}
+
+__device__ __forceinline__ long long quantize(float x, int K) {
+    return __double2ll_rn(ldexp(static_cast<double>(x), K));
+}
+
+// Apply the rows of locally moved documents: warp per document, lanes over its
+// nonzeros (distinct terms, so no intra-row conflicts); integer atomics only.
+__global__ void delta_local_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                   const float* __restrict__ val, const uint32_t* __restrict__ moved,
+                                   const unsigned long long* n_moved_p, const uint32_t* __restrict__ a,
+                                   uint32_t* __restrict__ a_sum, long long* __restrict__ S,
+                                   uint64_t ld, int K, uint8_t* __restrict__ touched) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    const uint64_t n_moved = *n_moved_p;
+    for (uint64_t m = gw; m < n_moved; m += nw) {
+        const uint32_t i = moved[m];
+        const uint32_t nc = a[i], oc = a_sum[i];
+        const int64_t beg = indptr[i], end = indptr[i + 1];
+        for (int64_t e = beg + lane; e < end; e += kWarp) {
+            const long long q = quantize(val[e], K);
+            const uint64_t row = static_cast<uint64_t>(idx[e]) * ld;
+            atomicAdd(reinterpret_cast<unsigned long long*>(S + row + nc),
+                      static_cast<unsigned long long>(q));
+            if (oc != kNone)
+                atomicAdd(reinterpret_cast<unsigned long long*>(S + row + oc),
+                          static_cast<unsigned long long>(-q));
+        }
+        __syncwarp();
+        if (lane == 0) {
+            touched[nc] = 1;
+            if (oc != kNone) touched[oc] = 1;
+            a_sum[i] = nc;
+        }
+    }
+}
+
+// Same for rows gathered from all ranks (multi-GPU delta exchange): packed
+// (old, new, row_ptr, idx, val) records, any order.
+__global__ void delta_packed_kernel(int64_t n_moved, const uint32_t* __restrict__ old_c,
+                                    const uint32_t* __restrict__ new_c,
+                                    const int64_t* __restrict__ row_ptr,
+                                    const int32_t* __restrict__ idx, const float* __restrict__ val,
+                                    long long* __restrict__ S, uint64_t ld, int K,
+                                    uint8_t* __restrict__ touched) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t m = gw; m < static_cast<uint64_t>(n_moved); m += nw) {
+        const uint32_t nc = new_c[m], oc = old_c[m];
+        for (int64_t e = row_ptr[m] + lane; e < row_ptr[m + 1]; e += kWarp) {
+            const long long q = quantize(val[e], K);
+            const uint64_t row = static_cast<uint64_t>(idx[e]) * ld;
+            atomicAdd(reinterpret_cast<unsigned long long*>(S + row + nc),
+                      static_cast<unsigned long long>(q));
+            if (oc != kNone)
+                atomicAdd(reinterpret_cast<unsigned long long*>(S + row + oc),
+                          static_cast<unsigned long long>(-q));
+        }
+        if (lane == 0) {
+            touched[nc] = 1;
+            if (oc != kNone) touched[oc] = 1;
+        }
+    }
+}
+
+// Ascending compaction of {j : flag(j)} in one block (k ≤ a few 1e5).
+// want = 1: keep flag != 0; want = 0: keep flag == 0.
+__global__ void compact_ids_kernel(const uint8_t* __restrict__ flags, uint32_t k, int want,
+                                   uint32_t* __restrict__ ids, unsigned int* n_out) {
+    __shared__ unsigned int warp_sums[32];
+    __shared__ unsigned int base;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (uint32_t j0 = 0; j0 < k; j0 += blockDim.x) {
+        const uint32_t j = j0 + threadIdx.x;
+        const unsigned int f = (j < k) && ((flags[j] != 0) == (want != 0));
+        const unsigned int bal = __ballot_sync(0xFFFFFFFFu, f);
+        const unsigned int pre = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) warp_sums[wid] = __popc(bal);
+        __syncthreads();
+        unsigned int off = 0;
+        for (int w = 0; w < wid; ++w) off += warp_sums[w];
+        if (f) ids[base + off + pre] = j;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned int tot = 0;
+            for (int w = 0; w < nwarps; ++w) tot += warp_sums[w];
+            base += tot;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_out = base;
+}
+
+constexpr int kRowBlock = 512;  // rows per partial in the column reductions
+
+// Σ_t S[t][j]² per recomputed column j, as fixed-order partials over row blocks.
+__global__ void norm2_partial_kernel(const long long* __restrict__ S, uint64_t ld, uint32_t d,
+                                     const uint32_t* __restrict__ ids, uint32_t n_ids,
+                                     double* __restrict__ part) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t rb = blockIdx.y;
+    if (c >= n_ids) return;
+    const uint32_t j = ids[c];
+    const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
+    double s = 0.0;
+    for (uint32_t t = t0; t < t1; ++t) {
+        const double v = static_cast<double>(S[static_cast<uint64_t>(t) * ld + j]);
+        s = fma(v, v, s);
+    }
+    part[static_cast<uint64_t>(rb) * n_ids + c] = s;
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ part, uint32_t n_rb,
+                                       uint32_t n_ids, double* __restrict__ out) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_ids) return;
+    double s = 0.0;
+    for (uint32_t rb = 0; rb < n_rb; ++rb) s += part[static_cast<uint64_t>(rb) * n_ids + c];
+    out[c] = s;
+}
+
+// Rewrite recomputed columns: c = S / ||S|| (fp64 division, then fp32), with
+// the squared drift against the previous fp32 column as fixed-order partials.
+__global__ void write_cols_kernel(const long long* __restrict__ S, float* __restrict__ CT,
+                                  uint64_t ld, uint32_t d, const uint32_t* __restrict__ ids,
+                                  uint32_t n_ids, const double* __restrict__ norm2,
+                                  double* __restrict__ part, unsigned int* zero_flag) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t rb = blockIdx.y;
+    if (c >= n_ids) return;
+    const uint32_t j = ids[c];
+    const double nrm = sqrt(norm2[c]);
+    if (nrm == 0.0) {  // normalize() of the zero vector throws (sparse_vector.cpp:161)
+        if (rb == 0) atomicOr(zero_flag, 1u);
+        return;
+    }
+    const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
+    double dr = 0.0;
+    for (uint32_t t = t0; t < t1; ++t) {
+        const uint64_t o = static_cast<uint64_t>(t) * ld + j;
+        const float cn = static_cast<float>(static_cast<double>(S[o]) / nrm);
+        const double diff = static_cast<double>(cn) - static_cast<double>(CT[o]);
+        dr = fma(diff, diff, dr);
+        CT[o] = cn;
+    }
+    part[static_cast<uint64_t>(rb) * n_ids + c] = dr;
+}
+
+// unchanged flags (detect_unchanged + repaired-forces-changed + iteration-1
+// rule, engine.cpp:366-376) and max drift.
+__global__ void flags_kernel(uint32_t k, int first_iter, double eps, const uint8_t* __restrict__ touched,
+                             const uint8_t* __restrict__ repaired, const uint32_t* __restrict__ rec_pos,
+                             const double* __restrict__ drift_rec, uint8_t* __restrict__ unchanged,
+                             double* __restrict__ drift_out, unsigned long long* max_drift_bits,
+                             unsigned int* n_unchanged) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+        double dj = 0.0;
+        if (touched[j]) dj = drift_rec[rec_pos[j]];
+        drift_out[j] = dj;
+        uint8_t u;
+        if (first_iter) {
+            u = 0;
+        } else {
+            u = (dj <= eps) ? 1 : 0;
+            if (repaired[j]) u = 0;
+            atomicMax(max_drift_bits, static_cast<unsigned long long>(__double_as_longlong(dj)));
+        }
+        unchanged[j] = u;
+        if (u) atomicAdd(n_unchanged, 1u);
+    }
+}
+
+__global__ void scatter_pos_kernel(const uint32_t* __restrict__ ids, uint32_t n, uint32_t* __restrict__ pos) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+        pos[ids[c]] = c;
+}
+
+// Compact copy of the changed columns for the NCC scan: CC[t][c] = Cᵀ[t][ids[c]],
+// zero-padded to ld_cc.
+__global__ void gather_cols_kernel(const float* __restrict__ CT, uint64_t ld, uint32_t d,
+                                   const uint32_t* __restrict__ ids, uint32_t n_ids,
+                                   float* __restrict__ CC, uint64_t ld_cc) {
+    const uint64_t total = static_cast<uint64_t>(d) * ld_cc;
+    for (uint64_t o = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; o < total;
+         o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t t = o / ld_cc;
+        const uint32_t c = static_cast<uint32_t>(o - t * ld_cc);
+        CC[o] = c < n_ids ? CT[t * ld + ids[c]] : 0.f;
+    }
+}
+
+// Seed init (BASELINE): Cᵀ[:, j] = row of document seeds[j] (values as stored).
+__global__ void scatter_seeds_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                     const float* __restrict__ val, const uint32_t* __restrict__ seeds,
+                                     uint32_t k, float* __restrict__ CT, uint64_t ld) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const uint32_t nw = gridDim.x * blockDim.x / kWarp;
+    for (uint32_t j = gw; j < k; j += nw) {
+        const uint32_t s = seeds[j];
+        for (int64_t e = indptr[s] + lane; e < indptr[s + 1]; e += kWarp)
+            CT[static_cast<uint64_t>(idx[e]) * ld + j] = val[e];
+    }
+}
+
+// CSR validation: indices strictly ascending within a row and < dims, values
+// nonzero, finite and |x| <= 1 (unit-length rows; the fixed-point bound).
+__global__ void validate_csr_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                    const float* __restrict__ val, int64_t n, uint32_t dims,
+                                    unsigned int* bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t b = indptr[i], e = indptr[i + 1];
+        if (e < b) {
+            atomicOr(bad, 1u);
+            continue;
+        }
+        int32_t prev = -1;
+        for (int64_t p = b; p < e; ++p) {
+            const int32_t t = idx[p];
+            const float x = val[p];
+            if (t <= prev || t < 0 || static_cast<uint32_t>(t) >= dims) atomicOr(bad, 2u);
+            if (x == 0.f) atomicOr(bad, 4u);
+            if (!(fabsf(x) <= 1.0f)) atomicOr(bad, 8u);
+            prev = t;
+        }
+    }
+}
+
+// k-means++ round (engine.cpp:86-96): sim_i = dot(x_i, seed) with the seed
+// scattered densely; strictly-greater update keeps the lowest cluster id.
+__global__ void kpp_round_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                 const float* __restrict__ val, int64_t n,
+                                 const float* __restrict__ dense_seed, uint32_t cluster,
+                                 uint32_t* __restrict__ a, double* __restrict__ sims) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t i = gw; i < static_cast<uint64_t>(n); i += nw) {
+        const int64_t beg = indptr[i], end = indptr[i + 1];
+        double s = 0.0;
+        for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
+            const int64_t e = e0 + lane;
+            float x_l = 0.f, c_l = 0.f;
+            if (e < end) {
+                x_l = val[e];
+                c_l = dense_seed[idx[e]];
+            }
+            const int cnt = static_cast<int>(imin64(kWarp, end - e0));
+            for (int j = 0; j < cnt; ++j) {
+                const double x = static_cast<double>(__shfl_sync(0xFFFFFFFFu, x_l, j));
+                const double c = static_cast<double>(__shfl_sync(0xFFFFFFFFu, c_l, j));
+                s = fma(x, c, s);
+            }
+        }
+        if (lane == 0 && s > sims[i]) {
+            sims[i] = s;
+            a[i] = cluster;
+        }
+    }
+}
+
+__global__ void scatter_row_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                   const float* __restrict__ val, int64_t row, float* __restrict__ dense,
+                                   int clear) {
+    for (int64_t e = indptr[row] + threadIdx.x; e < indptr[row + 1]; e += blockDim.x)
+        dense[idx[e]] = clear ? 0.f : val[e];
+}
+
+__global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void fill_f64_kernel(double* p, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void local_sum_kernel(const double* __restrict__ x, int64_t n, double* part) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    const int64_t per = ceil_div(n, gridDim.x);
+    const int64_t b0 = blockIdx.x * per, b1 = imin64(n, b0 + per);
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s += x[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+}  // namespace sskm_b200
