@@ -73,6 +73,7 @@ typedef struct {
     uint32_t n_changed;       /* centroids scanned by the NCC pass (unchanged flag clear) */
     uint32_t n_recomputed;    /* centroid columns rewritten by the update */
     uint64_t n_rescan;        /* NCC documents that needed the unchanged-centroid pass */
+    uint64_t n_exact;         /* documents the fp32 screen could not certify (exact fp64 scan) */
     double update_ms;         /* device time of compute_centroids + detect_unchanged */
     double assign_ms;         /* device time of the assignment step */
     double assign_kernel_ms;  /* device time of the dominant assign kernel(s) only */

@@ -52,6 +52,7 @@ class sskm_iteration_stats(C.Structure):
         ("n_changed", C.c_uint32),
         ("n_recomputed", C.c_uint32),
         ("n_rescan", C.c_uint64),
+        ("n_exact", C.c_uint64),
         ("update_ms", C.c_double),
         ("assign_ms", C.c_double),
         ("assign_kernel_ms", C.c_double),

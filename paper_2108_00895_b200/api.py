@@ -111,6 +111,7 @@ class IterationStats:
     n_changed: int = 0
     n_recomputed: int = 0
     n_rescan: int = 0
+    n_exact: int = 0
     update_ms: float = 0.0
     assign_ms: float = 0.0
     assign_kernel_ms: float = 0.0

@@ -20,65 +20,82 @@
 namespace sskm_b200 {
 
 template <int V>
-__device__ __forceinline__ void load_row(const float* __restrict__ p, float (&c)[V]) {
+struct VecT;
+template <>
+struct VecT<1> {
+    using type = float;
+};
+template <>
+struct VecT<2> {
+    using type = float2;
+};
+template <>
+struct VecT<4> {
+    using type = float4;
+};
+
+template <int V>
+__device__ __forceinline__ void unpack(const typename VecT<V>::type& t, float (&c)[V]) {
     if constexpr (V == 4) {
-        float4 t = __ldg(reinterpret_cast<const float4*>(p));
         c[0] = t.x;
         c[1] = t.y;
         c[2] = t.z;
         c[3] = t.w;
     } else if constexpr (V == 2) {
-        float2 t = __ldg(reinterpret_cast<const float2*>(p));
         c[0] = t.x;
         c[1] = t.y;
     } else {
-        c[0] = __ldg(p);
+        c[0] = t;
     }
 }
 
 // Per-lane fp64 partial dots of one document against columns
 // [col0 + lane·V, col0 + lane·V + V) of M, in ascending entry order.
-template <int V>
+//
+// Rows are addressed in V-float vector units with a 32-bit per-entry offset
+// (t · ld/V) computed once per entry by its owning lane, so the hot loop is one
+// shuffle + one wide load per entry. Loads are issued U at a time ahead of
+// their consumers (a compiler barrier keeps ptxas from re-interleaving them),
+// giving U independent L2 requests in flight per warp. The last batch of a
+// 32-entry chunk runs over lanes past the row end with x = 0, which adds exact
+// zeros and so leaves every fp64 sum bit-identical.
+template <int V, int U>
 __device__ __forceinline__ void doc_tile_dots(const int32_t* __restrict__ idx,
                                               const float* __restrict__ val, int64_t beg,
                                               int64_t end, const float* __restrict__ M,
                                               uint64_t ld, uint32_t col0, int lane,
                                               double (&acc)[V]) {
+    using VT = typename VecT<V>::type;
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = 0.0;
-    const float* base = M + col0 + static_cast<uint32_t>(lane) * V;
+    const VT* base = reinterpret_cast<const VT*>(M + col0) + lane;
+    const uint32_t ldv = static_cast<uint32_t>(ld / V);
     for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
         const int64_t e = e0 + lane;
-        int t_l = 0;
+        uint32_t off_l = 0;
         float x_l = 0.f;
         if (e < end) {
-            t_l = __ldg(idx + e);
+            off_l = static_cast<uint32_t>(__ldg(idx + e)) * ldv;
             x_l = __ldg(val + e);
         }
         const int n = static_cast<int>(imin64(kWarp, end - e0));
-        constexpr int U = 8;
-        int j = 0;
-        for (; j + U <= n; j += U) {
-            float c[U][V];
+        for (int j = 0; j < n; j += U) {
+            VT c[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int t = __shfl_sync(0xFFFFFFFFu, t_l, j + u);
-                load_row<V>(base + static_cast<uint64_t>(t) * ld, c[u]);
+                const uint32_t off = __shfl_sync(0xFFFFFFFFu, off_l, (j + u) & (kWarp - 1));
+                c[u] = __ldg(base + off);
             }
+            asm volatile("" ::: "memory");
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const double x = static_cast<double>(__shfl_sync(0xFFFFFFFFu, x_l, j + u));
+                const double x = static_cast<double>(__shfl_sync(0xFFFFFFFFu, x_l, (j + u) & (kWarp - 1)));
+                float cf[V];
+                unpack<V>(c[u], cf);
+                // lanes j+u >= n hold x = 0 (past the row end): exact no-ops
 #pragma unroll
-                for (int v = 0; v < V; ++v) acc[v] = fma(x, static_cast<double>(c[u][v]), acc[v]);
+                for (int v = 0; v < V; ++v) acc[v] = fma(x, static_cast<double>(cf[v]), acc[v]);
             }
-        }
-        for (; j < n; ++j) {
-            const int t = __shfl_sync(0xFFFFFFFFu, t_l, j);
-            const double x = static_cast<double>(__shfl_sync(0xFFFFFFFFu, x_l, j));
-            float c[V];
-            load_row<V>(base + static_cast<uint64_t>(t) * ld, c);
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[v] = fma(x, static_cast<double>(c[v]), acc[v]);
         }
     }
 }
@@ -108,103 +125,541 @@ __device__ __forceinline__ double doc_col_dot(const int32_t* __restrict__ idx,
     return s;
 }
 
-// Scan one document against `ncols` columns of M (column c is cluster
-// col_ids ? col_ids[c] : c), folding into (best, arg) under the tie rule.
-template <int V>
-__device__ __forceinline__ void scan_columns(const int32_t* __restrict__ idx,
-                                             const float* __restrict__ val, int64_t beg,
-                                             int64_t end, const float* __restrict__ M, uint64_t ld,
-                                             uint32_t ncols, const uint32_t* __restrict__ col_ids,
-                                             int lane, double& best, uint32_t& arg) {
-    for (uint32_t col0 = 0; col0 < ncols; col0 += kWarp * V) {
-        double acc[V];
-        doc_tile_dots<V>(idx, val, beg, end, M, ld, col0, lane, acc);
-        double lb = best;
-        uint32_t la = arg;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const uint32_t col = col0 + static_cast<uint32_t>(lane) * V + v;
-            if (col < ncols) {
-                const uint32_t id = col_ids ? __ldg(col_ids + col) : col;
-                if (better(acc[v], id, lb, la)) {
-                    lb = acc[v];
-                    la = id;
-                }
-            }
-        }
-        warp_argmax(lb, la);
-        best = lb;
-        arg = la;
-    }
-}
-
 enum ScanInit : int {
     kInitFull = 0,    // best = -2, arg = 0 (engine.cpp:252-253), all columns
     kInitNcc = 1,     // NCC pass A: cache or refreshed own dot, changed columns only
     kInitRescan = 2,  // NCC pass B: from pass A's result, all columns
 };
 
-struct AssignArgs {
+// One column tile of one assignment pass. The pass over all k columns is
+// issued tile-major (one launch per tile) so that the tile's slice of Cᵀ —
+// d × W fp32, sized to stay resident in the 126 MB L2 — is streamed from HBM
+// about once per iteration while the CSR rows stream past it; the per-document
+// running (best, arg) lives in a[] / sims[] between tiles.
+struct TileArgs {
     const int64_t* indptr;
     const int32_t* idx;
     const float* val;
     const float* M;            // matrix scanned (Cᵀ, or the compact changed-column copy)
     uint64_t ld;               // row stride of M
-    uint32_t ncols;            // columns of M to scan
+    uint32_t col0;             // first column of this tile
+    uint32_t ncols;            // total columns of M (tile may be partial)
     const uint32_t* col_ids;   // cluster id per column of M (nullptr = identity)
+    const uint32_t* order;     // work item -> document (nullptr = identity)
+    int64_t n_work;
+    int first, last;           // first / last tile of the pass
+    uint32_t* a;               // running argmax (in/out)
+    double* sims;              // running max (in/out)
+    // NCC pass A
+    const uint8_t* unchanged;  // per cluster
+    const uint32_t* a_start;   // assignment at the start of the step
+    const double* sims_start;  // cached sims at the start of the step
     const float* CT;           // full Cᵀ (own-centroid refresh)
     uint64_t ld_ct;
-    const uint32_t* doc_list;  // documents to process (nullptr = 0..n_work-1)
-    int64_t n_work;
-    const uint8_t* unchanged;  // per cluster
-    uint32_t* a;
-    double* sims;
-    uint32_t* rescan_list;     // pass A output
+    uint32_t* rescan_list;
     unsigned long long* n_rescan;
 };
 
-template <int V, int INIT>
-__global__ void __launch_bounds__(256) assign_kernel(AssignArgs p) {
+template <int V, int INIT, int U>
+__global__ void __launch_bounds__(256, 2) assign_tile_kernel(TileArgs p) {
     const int lane = threadIdx.x & (kWarp - 1);
-    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
-    for (uint64_t w = gw; w < static_cast<uint64_t>(p.n_work); w += nw) {
-        const int64_t i = p.doc_list ? static_cast<int64_t>(p.doc_list[w]) : static_cast<int64_t>(w);
+    const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
+    // contiguous chunk of the (cluster-ordered) work list per block: warps of a
+    // block, resident on one SM, share the hot rows of their cluster in L1
+    const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_work, gridDim.x));
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
+    const int64_t w1 = imin64(p.n_work, w0 + chunk);
+    for (int64_t w = w0 + warp; w < w1; w += nwarps) {
+        const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + w)) : w;
         const int64_t beg = __ldg(p.indptr + i), end = __ldg(p.indptr + i + 1);
         double best;
         uint32_t arg;
-        bool own_changed = false;
-        double old_sim = 0.0;
-        if constexpr (INIT == kInitFull) {
-            best = -2.0;
-            arg = 0;
-        } else if constexpr (INIT == kInitRescan) {
+        if (!p.first || INIT == kInitRescan) {
             best = p.sims[i];
             arg = p.a[i];
+        } else if constexpr (INIT == kInitFull) {
+            best = -2.0;
+            arg = 0;
         } else {
-            const uint32_t old_a = p.a[i];
-            old_sim = p.sims[i];
-            own_changed = p.unchanged[old_a] == 0;
+            const uint32_t old_a = p.a_start[i];
+            const bool own_changed = p.unchanged[old_a] == 0;
             // unchanged own centroid: the cache is current (engine.cpp:268-270);
             // otherwise refresh the baseline (engine.cpp:271-273)
             best = own_changed ? doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, old_a, lane)
-                               : old_sim;
+                               : p.sims_start[i];
             arg = old_a;
         }
-        scan_columns<V>(p.idx, p.val, beg, end, p.M, p.ld, p.ncols, p.col_ids, lane, best, arg);
+        {
+            double acc[V];
+            doc_tile_dots<V, U>(p.idx, p.val, beg, end, p.M, p.ld, p.col0, lane, acc);
+            double lb = best;
+            uint32_t la = arg;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const uint32_t col = p.col0 + static_cast<uint32_t>(lane) * V + v;
+                if (col < p.ncols) {
+                    const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
+                    if (better(acc[v], id, lb, la)) {
+                        lb = acc[v];
+                        la = id;
+                    }
+                }
+            }
+            warp_argmax(lb, la);
+            best = lb;
+            arg = la;
+        }
         if (lane == 0) {
             p.a[i] = arg;
             p.sims[i] = best;
             if constexpr (INIT == kInitNcc) {
                 // the refreshed scan did not beat the cached max: unchanged
                 // centroids may tie or exceed it (engine.cpp:303-305)
-                if (own_changed && !(best > old_sim)) {
-                    const unsigned long long pos = atomicAdd(p.n_rescan, 1ull);
-                    p.rescan_list[pos] = static_cast<uint32_t>(i);
+                if (p.last) {
+                    const uint32_t old_a = p.a_start[i];
+                    if (p.unchanged[old_a] == 0 && !(best > p.sims_start[i])) {
+                        const unsigned long long pos = atomicAdd(p.n_rescan, 1ull);
+                        p.rescan_list[pos] = static_cast<uint32_t>(i);
+                    }
                 }
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Screened scan: fp32 FFMA over the tile, exact fp64 only where needed.
+//
+// The fp64 similarity the reference computes and an fp32 FMA accumulation of
+// the same products differ by at most
+//     δ_i = (γ32(n_i) + γ64(n_i)) · ||x_i||₂ · max_j ||c_j||₂,   γ(n) = n·u/(1−n·u)
+// (sequential summation bound with Σ|x_t c_t| ≤ ||x||·||c||). The screen keeps,
+// per document, the fp32 best, its column and the fp32 runner-up across all
+// tiles. When best − runner-up > 2δ the fp32 winner is the unique fp64 argmax
+// (no tie possible), and its similarity is then recomputed exactly in fp64 in
+// ascending term order — bit-identical to the reference. Documents the screen
+// cannot certify take the exact fp64 scan. The hot loop is thus one shuffle,
+// one wide load and V FFMAs per entry: no fp32->fp64 conversions (the XU pipe
+// they run on is quarter rate) and half the register footprint.
+// ---------------------------------------------------------------------------
+
+// L2 eviction policies: the CSR streams past (evict_first, no L1
+// allocation) while the current column tile of Cᵀ is kept (evict_last).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 ld_keep(const float4* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float2 ld_keep(const float2* p, uint64_t pol) {
+    float2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_keep(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+template <int V, int U>
+__device__ __forceinline__ void doc_tile_dots32(const int32_t* __restrict__ idx,
+                                                const float* __restrict__ val, int64_t beg,
+                                                int64_t end, const float* __restrict__ M,
+                                                uint64_t ld, uint32_t col0, int lane,
+                                                uint64_t pol_keep, uint64_t pol_stream,
+                                                float (&acc)[V]) {
+    using VT = typename VecT<V>::type;
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = 0.f;
+    const VT* base = reinterpret_cast<const VT*>(M + col0) + lane;
+    const uint32_t ldv = static_cast<uint32_t>(ld / V);
+    for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
+        const int64_t e = e0 + lane;
+        uint32_t off_l = 0;
+        float x_l = 0.f;
+        if (e < end) {
+            off_l = static_cast<uint32_t>(ld_stream_i32(idx + e, pol_stream)) * ldv;
+            x_l = ld_stream_f32(val + e, pol_stream);
+        }
+        const int n = static_cast<int>(imin64(kWarp, end - e0));
+        // fully unrolled over the 32-entry chunk: shuffle source lanes are
+        // immediates; batches past n are skipped, lanes >= n carry x = 0
+#pragma unroll
+        for (int j = 0; j < kWarp; j += U) {
+            if (j >= n) break;
+            VT c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t off = __shfl_sync(0xFFFFFFFFu, off_l, j + u);
+                c[u] = ld_keep(base + off, pol_keep);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const float x = __shfl_sync(0xFFFFFFFFu, x_l, j + u);
+                float cf[V];
+                unpack<V>(c[u], cf);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = fmaf(x, cf[v], acc[v]);
+            }
+        }
+    }
+}
+
+// (best, arg, second) fold; equal bests make second == best (uncertified).
+__device__ __forceinline__ void top2_push(float s, uint32_t id, float& b, uint32_t& a, float& s2) {
+    if (s > b || (s == b && id < a)) {
+        s2 = fmaxf(s2, b);
+        b = s;
+        a = id;
+    } else {
+        s2 = fmaxf(s2, s);
+    }
+}
+
+__device__ __forceinline__ void warp_top2(float& b, uint32_t& a, float& s2) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float ob = __shfl_xor_sync(0xFFFFFFFFu, b, off);
+        const uint32_t oa = __shfl_xor_sync(0xFFFFFFFFu, a, off);
+        const float os2 = __shfl_xor_sync(0xFFFFFFFFu, s2, off);
+        if (ob > b || (ob == b && oa < a)) {
+            s2 = fmaxf(os2, b);
+            b = ob;
+            a = oa;
+        } else {
+            s2 = fmaxf(s2, ob);
+        }
+    }
+}
+
+struct ScreenArgs {
+    const int64_t* indptr;
+    const int32_t* idx;
+    const float* val;
+    const float* M;
+    uint64_t ld;
+    uint32_t col0;
+    uint32_t ncols;
+    const uint32_t* col_ids;   // nullptr = identity
+    const uint32_t* order;     // work item -> document
+    int64_t n_work;
+    int first;
+    const uint32_t* skip_id;   // per document: cluster excluded from the screen (NCC own), or nullptr
+    float* sb;                 // running fp32 best   (per document)
+    float* ss;                 // running fp32 second
+    uint32_t* sa;              // running fp32 argmax (kNone = no candidate)
+};
+
+template <int V, int U>
+__global__ void __launch_bounds__(256, 2) screen_tile_kernel(ScreenArgs p) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
+    const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_work, gridDim.x));
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
+    const int64_t w1 = imin64(p.n_work, w0 + chunk);
+    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+    for (int64_t w = w0 + warp; w < w1; w += nwarps) {
+        const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + w)) : w;
+        const int64_t beg = __ldg(p.indptr + i), end = __ldg(p.indptr + i + 1);
+        const uint32_t skip = p.skip_id ? __ldg(p.skip_id + i) : kNone;
+        float b = -INFINITY, s2 = -INFINITY;
+        uint32_t a = kNone;
+        if (!p.first) {
+            b = p.sb[i];
+            s2 = p.ss[i];
+            a = p.sa[i];
+        }
+        float acc[V];
+        doc_tile_dots32<V, U>(p.idx, p.val, beg, end, p.M, p.ld, p.col0, lane, pol_keep, pol_stream, acc);
+        float lb = -INFINITY, ls2 = -INFINITY;
+        uint32_t la = kNone;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const uint32_t col = p.col0 + static_cast<uint32_t>(lane) * V + v;
+            if (col < p.ncols) {
+                const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
+                if (id != skip) top2_push(acc[v], id, lb, la, ls2);
+            }
+        }
+        warp_top2(lb, la, ls2);
+        if (lane == 0) {
+            if (la != kNone) {
+                top2_push(lb, la, b, a, s2);
+                s2 = fmaxf(s2, ls2);
+            }
+            p.sb[i] = b;
+            p.ss[i] = s2;
+            p.sa[i] = a;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Postings screen: the centroid matrix as an inverted index.
+//
+// Centroids are ~7% dense on the BASELINE corpora (most terms occur in few
+// clusters), so the dense scan spends >90% of its bytes on zeros. The postings
+// view stores, per cluster tile T (KT clusters) and term t, the list of
+// (cluster, value) pairs with a nonzero centroid weight — the paper's index
+// over centroids (§3.2) in GPU form. A warp owns one document and a
+// KT-float accumulator in shared memory; for each of the document's terms in
+// ascending order, the 32 lanes stride over that term's posting list and do
+// acc[c] = fma(x_t, v, acc[c]). Clusters within one list are distinct, so no
+// atomics are needed (a __syncwarp orders consecutive lists). The fp32 result
+// per (doc, cluster) is the same ascending-term FMA chain as the dense screen,
+// so the same certification bound applies.
+// ---------------------------------------------------------------------------
+struct PostingsArgs {
+    const int64_t* indptr;
+    const int32_t* idx;
+    const float* val;
+    const int64_t* pptr;       // d + 1 offsets into pairs for this cluster tile
+    const uint2* pairs;        // (local cluster, float bits)
+    uint32_t c0;               // first column of the tile (in M's column space)
+    uint32_t kt;               // columns in this tile
+    const uint32_t* col_ids;   // column -> cluster id (nullptr = identity)
+    const uint32_t* order;
+    int64_t n_work;
+    int first;
+    const uint32_t* skip_id;
+    float* sb;
+    float* ss;
+    uint32_t* sa;
+};
+
+template <int KT>
+__global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
+    extern __shared__ float smem_acc[];
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
+    float* acc = smem_acc + static_cast<size_t>(warp) * KT;
+    const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_work, gridDim.x));
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
+    const int64_t w1 = imin64(p.n_work, w0 + chunk);
+    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+    for (int64_t w = w0 + warp; w < w1; w += nwarps) {
+        const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + w)) : w;
+        const int64_t beg = __ldg(p.indptr + i), end = __ldg(p.indptr + i + 1);
+        const uint32_t skip = p.skip_id ? __ldg(p.skip_id + i) : kNone;
+#pragma unroll
+        for (int c = lane * 4; c < KT; c += kWarp * 4)
+            *reinterpret_cast<float4*>(acc + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
+            const int64_t e = e0 + lane;
+            int64_t lb = 0, le = 0;
+            float x_l = 0.f;
+            if (e < end) {
+                const int32_t t = ld_stream_i32(p.idx + e, pol_stream);
+                x_l = ld_stream_f32(p.val + e, pol_stream);
+                lb = __ldg(p.pptr + t);
+                le = __ldg(p.pptr + t + 1);
+            }
+            const int n = static_cast<int>(imin64(kWarp, end - e0));
+            for (int j = 0; j < n; ++j) {
+                const int64_t b = __shfl_sync(0xFFFFFFFFu, lb, j);
+                const int64_t en = __shfl_sync(0xFFFFFFFFu, le, j);
+                const float x = __shfl_sync(0xFFFFFFFFu, x_l, j);
+                for (int64_t q = b + lane; q < en; q += kWarp) {
+                    uint2 pr;
+                    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                                 : "=r"(pr.x), "=r"(pr.y) : "l"(p.pairs + q), "l"(pol_keep));
+                    acc[pr.x] = fmaf(x, __uint_as_float(pr.y), acc[pr.x]);
+                }
+                __syncwarp();
+            }
+        }
+        // top-2 over the tile's clusters
+        float tb = -INFINITY, ts2 = -INFINITY;
+        uint32_t ta = kNone;
+        for (int c = lane; c < static_cast<int>(p.kt); c += kWarp) {
+            const uint32_t col = p.c0 + static_cast<uint32_t>(c);
+            const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
+            if (id != skip) top2_push(acc[c], id, tb, ta, ts2);
+        }
+        warp_top2(tb, ta, ts2);
+        if (lane == 0) {
+            float b = -INFINITY, s2 = -INFINITY;
+            uint32_t a = kNone;
+            if (!p.first) {
+                b = p.sb[i];
+                s2 = p.ss[i];
+                a = p.sa[i];
+            }
+            if (ta != kNone) {
+                top2_push(tb, ta, b, a, s2);
+                s2 = fmaxf(s2, ts2);
+            }
+            p.sb[i] = b;
+            p.ss[i] = s2;
+            p.sa[i] = a;
+        }
+        __syncwarp();
+    }
+}
+
+// Postings build from the dense column tile [c0, c0 + kt) of M: per-row counts,
+// then (after an exclusive scan) the pairs in ascending cluster order.
+__global__ void postings_count_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d, uint32_t c0,
+                                      uint32_t kt, int64_t* __restrict__ cnt) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t t = gw; t < d; t += nw) {
+        const float* row = M + t * ld + c0;
+        int c = 0;
+        for (uint32_t j = lane; j < kt; j += kWarp) c += row[j] != 0.f;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, off);
+        if (lane == 0) cnt[t] = c;
+    }
+}
+
+__global__ void postings_fill_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d, uint32_t c0,
+                                     uint32_t kt, const int64_t* __restrict__ pptr, uint2* __restrict__ pairs) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t t = gw; t < d; t += nw) {
+        const float* row = M + t * ld + c0;
+        int64_t pos = pptr[t];
+        for (uint32_t j0 = 0; j0 < kt; j0 += kWarp) {
+            const uint32_t j = j0 + lane;
+            const float v = j < kt ? row[j] : 0.f;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, v != 0.f);
+            if (v != 0.f) {
+                const int r = __popc(bal & ((1u << lane) - 1u));
+                pairs[pos + r] = make_uint2(j, __float_as_uint(v));
+            }
+            pos += __popc(bal);
+        }
+    }
+}
+
+struct ResolveArgs {
+    const int64_t* indptr;
+    const int32_t* idx;
+    const float* val;
+    const float* CT;
+    uint64_t ld_ct;
+    const uint32_t* order;
+    int64_t n_work;
+    double cmax;               // upper bound on every centroid column's 2-norm
+    const float* sb;
+    const float* ss;
+    const uint32_t* sa;
+    // NCC
+    const uint8_t* unchanged;
+    const uint32_t* a_start;
+    const double* sims_start;
+    uint32_t* a;
+    double* sims;
+    uint32_t* exact_list;      // uncertified documents -> exact fp64 scan
+    unsigned long long* n_exact;
+    uint32_t* rescan_list;
+    unsigned long long* n_rescan;
+};
+
+// Certify the screen's answer per document (warp per document).
+template <int INIT>
+__global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t w = gw; w < static_cast<uint64_t>(p.n_work); w += nw) {
+        const int64_t i = p.order ? static_cast<int64_t>(p.order[w]) : static_cast<int64_t>(w);
+        const int64_t beg = p.indptr[i], end = p.indptr[i + 1];
+        // ||x||₂ (fp64) for the error bound
+        double q = 0.0;
+        for (int64_t e = beg + lane; e < end; e += kWarp) {
+            const double x = static_cast<double>(p.val[e]);
+            q = fma(x, x, q);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, off);
+        const double n = static_cast<double>(end - beg);
+        const double u32 = 0x1p-24, u64 = 0x1p-53;
+        const double g32 = n * u32 / (1.0 - n * u32), g64 = n * u64 / (1.0 - n * u64);
+        const double delta = (g32 + g64) * sqrt(q) * (1.0 + 1e-12) * p.cmax * (1.0 + 1e-12);
+        const float b = p.sb[i], s2 = p.ss[i];
+        const uint32_t sa = p.sa[i];
+        double best;
+        uint32_t arg;
+        bool certain;
+        bool own_changed = false;
+        double old_sim = 0.0;
+        if constexpr (INIT == kInitFull) {
+            // the screen covered every column; the reference's (-2, 0) start only
+            // survives when every similarity is <= -2 (left to the exact scan)
+            certain = sa != kNone && static_cast<double>(b) - static_cast<double>(s2) > 2.0 * delta;
+            best = 0.0;
+            arg = sa;
+            if (certain) {
+                best = doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, sa, lane);
+                certain = best > -2.0;
+            }
+        } else {
+            const uint32_t a0 = p.a_start[i];
+            old_sim = p.sims_start[i];
+            own_changed = p.unchanged[a0] == 0;
+            const double sim0 = own_changed ? doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, a0, lane)
+                                            : old_sim;
+            best = sim0;
+            arg = a0;
+            if (sa == kNone || static_cast<double>(b) < sim0 - delta) {
+                certain = true;  // no screened column can reach the baseline
+            } else if (static_cast<double>(b) - delta > sim0 &&
+                       static_cast<double>(b) - static_cast<double>(s2) > 2.0 * delta) {
+                best = doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, sa, lane);
+                arg = sa;
+                certain = true;
+            } else {
+                certain = false;
+            }
+        }
+        if (lane == 0) {
+            if (certain) {
+                p.a[i] = arg;
+                p.sims[i] = best;
+                if constexpr (INIT == kInitNcc) {
+                    if (own_changed && !(best > old_sim)) {  // engine.cpp:303-305
+                        const unsigned long long pos = atomicAdd(p.n_rescan, 1ull);
+                        p.rescan_list[pos] = static_cast<uint32_t>(i);
+                    }
+                }
+            } else {
+                const unsigned long long pos = atomicAdd(p.n_exact, 1ull);
+                p.exact_list[pos] = static_cast<uint32_t>(i);
+            }
+        }
+    }
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ p, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = static_cast<uint32_t>(i);
 }
 
 // Σ sims (fixed-shape tree: bitwise reproducible for a given n) and the

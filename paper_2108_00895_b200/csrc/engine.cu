@@ -10,12 +10,15 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <random>
 #include <string>
 #include <vector>
+
+#include <cub/cub.cuh>
 
 #include "../../include/sskm_b200.h"
 #include "assign_kernels.cuh"
@@ -32,6 +35,7 @@ struct InvalidArgument : std::invalid_argument {
 struct Scalars {
     unsigned long long n_moved;
     unsigned long long n_rescan;
+    unsigned long long n_exact;
     unsigned long long reassigned;
     unsigned long long max_drift_bits;
     unsigned long long donor_key;
@@ -74,11 +78,23 @@ public:
         CK(cudaGetDeviceProperties(&prop, device));
         if (prop.major != 10) throw CudaError("sskm_b200 requires an sm_100 (B200) device");
         sms_ = prop.multiProcessorCount;
+        if (const char* e = std::getenv("SSKM_TILE_BYTES")) tile_bytes_ = std::strtoull(e, nullptr, 10);
+        if (const char* e = std::getenv("SSKM_ORDER")) order_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_UNROLL")) unroll_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_SCREEN_UNROLL")) screen_unroll_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_SCREEN_KIND")) screen_kind_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_SCREEN")) screen_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_SCREEN_BLOCKS_PER_SM")) screen_blocks_per_sm_ = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("SSKM_BLOCKS_PER_SM")) blocks_per_sm_ = std::max(1, std::atoi(e));
         CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
         for (auto& e : ev_) CK(cudaEventCreate(&e));
         for (auto& e : user_ev_) CK(cudaEventCreate(&e));
         scal_.alloc(1);
         CK(cudaMallocHost(&hs_, sizeof(Scalars)));
+        // the screen keeps hot Cᵀ rows in L1: give L1 the whole carveout
+        for (auto k : {screen_tile_kernel<1, 8>, screen_tile_kernel<2, 8>, screen_tile_kernel<4, 8>,
+                       screen_tile_kernel<1, 16>, screen_tile_kernel<2, 16>, screen_tile_kernel<4, 16>})
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     }
 
     ~Engine() {
@@ -157,6 +173,7 @@ public:
         a_sum_.alloc(n);
         a_start_.alloc(n);
         sims_.alloc(n);
+        sims_start_.alloc(n);
         moved_.alloc(n);
         rescan_.alloc(n);
         corpus_ = true;
@@ -238,6 +255,7 @@ public:
         launch(scatter_seeds_kernel, grid_for(static_cast<int64_t>(k_) * 32, 256), 256, 
             indptr_.p, idx_.p, val_.p, dseeds.p, k_, ct_.p, ld_);
         CK_LAUNCH();
+        seed_cmax(dseeds.p);
         seed_assign_state();
         sskm_iteration_stats st{};
         full_assign(&st);
@@ -312,6 +330,7 @@ public:
         launch(scatter_seeds_kernel, grid_for(static_cast<int64_t>(k_) * 32, 256), 256, 
             indptr_.p, idx_.p, val_.p, dseeds.p, k_, ct_.p, ld_);
         CK_LAUNCH();
+        seed_cmax(dseeds.p);
         reset_sums();
         CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
         iteration_ = 0;
@@ -392,52 +411,54 @@ public:
 
     void full_assign(sskm_iteration_stats* st) {
         CK(cudaEventRecord(ev_[2], stream_));
-        CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
-        AssignArgs p = base_args();
-        p.M = ct_.p;
-        p.ld = ld_;
-        p.ncols = k_;
-        p.col_ids = nullptr;
-        p.doc_list = nullptr;
-        p.n_work = n_;
+        snapshot_start();
+        const uint32_t* order = cluster_order();
+        reset_scalars();
         CK(cudaEventRecord(ev_[4], stream_));
-        launch_scan<kInitFull>(p, k_);
+        uint64_t n_exact = 0;
+        if (screen_enabled_) {
+            screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_);
+            resolve<kInitFull>(order, n_);
+            pull_scalars();
+            n_exact = hs_->n_exact;
+            if (n_exact > 0) scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(n_exact));
+        } else {
+            scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, order, n_);
+        }
         CK(cudaEventRecord(ev_[5], stream_));
         finish_assign(st);
         st->n_unchanged_centroids = iteration_ <= 1 ? 0 : n_unchanged_;
         st->dot_products = static_cast<uint64_t>(k_) * static_cast<uint64_t>(n_);
-        st->gpu_dot_products = st->dot_products;
+        st->gpu_dot_products = st->dot_products + n_exact * k_;
         st->n_changed = k_;
         st->n_rescan = 0;
+        st->n_exact = n_exact;
         timing(st);
     }
 
     void ncc_assign(sskm_iteration_stats* st) {
         CK(cudaEventRecord(ev_[2], stream_));
-        CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+        snapshot_start();
         ensure_cc();
+        const uint32_t* order = cluster_order();
         reset_scalars();
-        AssignArgs p = base_args();
-        p.M = cc_.p;
-        p.ld = ld_cc_;
-        p.ncols = n_chg_;
-        p.col_ids = chg_ids_.p;
-        p.doc_list = nullptr;
-        p.n_work = n_;
         CK(cudaEventRecord(ev_[4], stream_));
-        launch_scan<kInitNcc>(p, n_chg_);
+        uint64_t n_exact = 0;
+        if (n_chg_ > 0) {
+            if (screen_enabled_) {
+                screen_any(cc_.p, ld_cc_, n_chg_, chg_ids_.p, a_start_.p, order, n_);
+                resolve<kInitNcc>(order, n_);
+                pull_scalars();
+                n_exact = hs_->n_exact;
+                if (n_exact > 0)
+                    scan_tiles<kInitNcc>(cc_.p, ld_cc_, n_chg_, chg_ids_.p, exact_.p, static_cast<int64_t>(n_exact));
+            } else {
+                scan_tiles<kInitNcc>(cc_.p, ld_cc_, n_chg_, chg_ids_.p, order, n_);
+            }
+        }
         pull_scalars();
         const uint64_t n_rescan = hs_->n_rescan;
-        if (n_rescan > 0) {
-            AssignArgs q = base_args();
-            q.M = ct_.p;
-            q.ld = ld_;
-            q.ncols = k_;
-            q.col_ids = nullptr;
-            q.doc_list = rescan_.p;
-            q.n_work = static_cast<int64_t>(n_rescan);
-            launch_scan<kInitRescan>(q, k_);
-        }
+        if (n_rescan > 0) scan_tiles<kInitRescan>(ct_.p, ld_, k_, nullptr, rescan_.p, static_cast<int64_t>(n_rescan));
         CK(cudaEventRecord(ev_[5], stream_));
         finish_assign(st);
         // dot accounting of the reference (engine.cpp:253-306): every document
@@ -447,9 +468,10 @@ public:
         const uint64_t n_unch = k_ - n_chg_;
         st->n_unchanged_centroids = static_cast<uint32_t>(n_unch);
         st->dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_rescan * n_unch;
-        st->gpu_dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_rescan * k_;
+        st->gpu_dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_exact * n_chg_ + n_rescan * k_;
         st->n_changed = n_chg_;
         st->n_rescan = n_rescan;
+        st->n_exact = n_exact;
         timing(st);
     }
 
@@ -495,6 +517,14 @@ public:
         CK(cudaMemsetAsync(ct_.p, 0, static_cast<uint64_t>(d_) * ld_ * 4, stream_));
         CK(cudaMemcpy2DAsync(ct_.p, ld_ * sizeof(float), ct, k_ * sizeof(float), k_ * sizeof(float), d_,
                              cudaMemcpyHostToDevice, stream_));
+        std::vector<double> nrm(k_, 0.0);
+        for (uint64_t t = 0; t < d_; ++t)
+            for (uint32_t j = 0; j < k_; ++j) {
+                const double c = ct[t * k_ + j];
+                nrm[j] += c * c;
+            }
+        cmax_ = 1e-300;
+        for (double q : nrm) cmax_ = std::max(cmax_, std::sqrt(q) * (1.0 + 1e-12));
         reset_sums();
         have_cc_ = false;
         CK(cudaStreamSynchronize(stream_));
@@ -624,6 +654,18 @@ private:
         CK(cudaStreamSynchronize(stream_));
     }
 
+    // Bound on the centroid column norms after a seed init (the screen's δ).
+    void seed_cmax(const uint32_t* dseeds) {
+        reset_scalars();
+        launch(seed_norm_max_kernel, grid_for(k_, 128), 128, indptr_.p, val_.p, dseeds, k_,
+               &scal_.p->max_drift_bits);
+        CK_LAUNCH();
+        pull_scalars();
+        double m;
+        std::memcpy(&m, &hs_->max_drift_bits, 8);
+        cmax_ = std::max(m, 1e-300) * (1.0 + 1e-12);
+    }
+
     void seed_assign_state() {
         launch(fill_u32_kernel, grid_for(n_, 256), 256, a_.p, n_, 0);
         launch(fill_f64_kernel, grid_for(n_, 256), 256, sims_.p, n_, -2.0);
@@ -661,36 +703,92 @@ private:
     }
 
     // Empty-cluster repair for one context (engine.cpp:154-167): ascending
-    // empty clusters, each taking the lowest-(sim, index) document from a
-    // cluster that can spare it. Rare path; host-sequenced small kernels.
+    // empty clusters, each taking the lowest-(sim, index) document among those
+    // whose cluster can spare one. One stable radix sort of (sim, doc) keys
+    // gives the candidates in the reference's scan order; the sequential rule
+    // (sizes shrink as donors leave) is then replayed exactly on the host over
+    // the first M candidates, doubling M in the (never observed) case that all
+    // of them become ineligible.
     void repair_empty_single() {
         launch(count_empty_kernel, grid_for(k_, 256), 256, counts_.p, k_, &scal_.p->n_empty);
         CK_LAUNCH();
         pull_scalars();
         if (hs_->bad) throw InvalidArgument("assignment out of range");
         CK(cudaMemsetAsync(repaired_flag_.p, 0, k_, stream_));
-        if (hs_->n_empty == 0) return;
+        const uint32_t n_empty = hs_->n_empty;
+        if (n_empty == 0) return;
         std::vector<unsigned long long> counts(k_);
         CK(cudaMemcpyAsync(counts.data(), counts_.p, k_ * 8, cudaMemcpyDeviceToHost, stream_));
-        CK(cudaStreamSynchronize(stream_));
+        sort_sim_candidates();
+        std::vector<uint32_t> moves;  // (doc, cluster) pairs
         std::vector<uint8_t> flag(k_, 0);
-        for (uint32_t j = 0; j < k_; ++j) {
-            if (counts[j] != 0) continue;
-            const uint64_t donor = find_donor();
-            if (donor == ULLONG_MAX) throw CudaError("empty-cluster repair found no donor");
-            uint32_t old_c;
-            CK(cudaMemcpyAsync(&old_c, a_.p + donor, 4, cudaMemcpyDeviceToHost, stream_));
-            CK(cudaStreamSynchronize(stream_));
-            --counts[old_c];
-            counts[j] = 1;
-            CK(cudaMemcpyAsync(a_.p + donor, &j, 4, cudaMemcpyHostToDevice, stream_));
-            CK(cudaMemcpyAsync(counts_.p + old_c, &counts[old_c], 8, cudaMemcpyHostToDevice, stream_));
-            CK(cudaMemcpyAsync(counts_.p + j, &counts[j], 8, cudaMemcpyHostToDevice, stream_));
-            CK(cudaStreamSynchronize(stream_));
-            repaired_.push_back(j);
-            flag[j] = 1;
+        uint64_t m = std::min<uint64_t>(n_, static_cast<uint64_t>(n_empty) * 2 + 256);
+        for (;;) {
+            std::vector<uint32_t> docs(m), cur(m);
+            fetch_candidates(m, docs.data(), cur.data());
+            std::vector<unsigned long long> cnt = counts;
+            std::vector<uint8_t> used(m, 0);
+            std::vector<uint32_t> mv;
+            bool ok = true;
+            uint64_t pos = 0;  // first candidate not yet used
+            for (uint32_t j = 0; j < k_ && ok; ++j) {
+                if (cnt[j] != 0) continue;
+                uint64_t c = pos;
+                while (c < m && (used[c] || cnt[cur[c]] < 2)) ++c;
+                if (c == m) {
+                    ok = false;
+                    break;
+                }
+                used[c] = 1;
+                while (pos < m && used[pos]) ++pos;
+                --cnt[cur[c]];
+                cur[c] = j;
+                cnt[j] = 1;
+                mv.push_back(docs[c]);
+                mv.push_back(j);
+            }
+            if (ok) {
+                moves.swap(mv);
+                break;
+            }
+            if (m == static_cast<uint64_t>(n_)) throw CudaError("empty-cluster repair found no donor");
+            m = std::min<uint64_t>(n_, m * 4);
         }
+        for (size_t q = 0; q < moves.size(); q += 2) {
+            repaired_.push_back(moves[q + 1]);
+            flag[moves[q + 1]] = 1;
+        }
+        DevBuf<uint32_t> dm;
+        dm.alloc(moves.size());
+        CK(cudaMemcpyAsync(dm.p, moves.data(), moves.size() * 4, cudaMemcpyHostToDevice, stream_));
+        launch(apply_moves_kernel, 1, 256, dm.p, static_cast<uint32_t>(moves.size() / 2), a_.p);
+        CK_LAUNCH();
         CK(cudaMemcpyAsync(repaired_flag_.p, flag.data(), k_, cudaMemcpyHostToDevice, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void sort_sim_candidates() {
+        keys_.alloc(2 * n_);
+        vals_.alloc(2 * n_);
+        launch(sim_keys_kernel, grid_for(n_, 256), 256, sims_.p, n_, keys_.p, vals_.p);
+        CK_LAUNCH();
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_.p, keys_.p + n_, vals_.p, vals_.p + n_,
+                                           static_cast<int>(n_), 0, 64, stream_));
+        sort_tmp_.alloc(tmp);
+        CK(cub::DeviceRadixSort::SortPairs(sort_tmp_.p, tmp, keys_.p, keys_.p + n_, vals_.p, vals_.p + n_,
+                                           static_cast<int>(n_), 0, 64, stream_));
+        ++launches_;
+    }
+
+    // First m candidates in (sim, doc) order and their current clusters.
+    void fetch_candidates(uint64_t m, uint32_t* docs, uint32_t* cur) {
+        launch(gather_assign_kernel, grid_for(m, 256), 256, vals_.p + n_, static_cast<uint32_t>(m), a_.p,
+               vals_.p);
+        CK_LAUNCH();
+        CK(cudaMemcpyAsync(docs, vals_.p + n_, m * 4, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(cur, vals_.p, m * 4, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
     }
 
     // Renormalise touched columns, drift, unchanged flags, changed list.
@@ -721,6 +819,8 @@ private:
         pull_scalars();
         if (hs_->zero_flag) throw InvalidArgument("cannot normalize zero vector");
         n_unchanged_ = hs_->n_unchanged;
+        // rewritten columns are fp32 roundings of unit vectors: ||c|| <= 1 + 2^-23
+        if (n_rec > 0) cmax_ = (n_rec == k_) ? 1.0 + 0x1p-22 : std::max(cmax_, 1.0 + 0x1p-22);
         double max_drift;
         std::memcpy(&max_drift, &hs_->max_drift_bits, 8);
         have_cc_ = false;
@@ -749,32 +849,256 @@ private:
         have_cc_ = true;
     }
 
-    AssignArgs base_args() const {
-        AssignArgs p{};
-        p.indptr = indptr_.p;
-        p.idx = idx_.p;
-        p.val = val_.p;
-        p.CT = ct_.p;
-        p.ld_ct = ld_;
-        p.unchanged = unchanged_.p;
-        p.a = a_.p;
-        p.sims = sims_.p;
-        p.rescan_list = rescan_.p;
-        p.n_rescan = &scal_.p->n_rescan;
-        return p;
+    void snapshot_start() {
+        CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+        CK(cudaMemcpyAsync(sims_start_.p, sims_.p, n_ * 8, cudaMemcpyDeviceToDevice, stream_));
+    }
+
+    // Documents ordered by their current cluster (stable): consecutive work
+    // items of a block then share their cluster's hot Cᵀ rows in L1. Pure
+    // scheduling — every document's result is independent of the order.
+    const uint32_t* cluster_order() {
+        if (!order_enabled_) return nullptr;
+        order_.alloc(2 * n_);
+        keys32_.alloc(n_);
+        launch(iota_kernel, grid_for(n_, 256), 256, order_.p, n_);
+        CK_LAUNCH();
+        int bits = 1;
+        while ((1u << bits) < k_ && bits < 32) ++bits;
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, a_.p, keys32_.p, order_.p, order_.p + n_,
+                                           static_cast<int>(n_), 0, bits, stream_));
+        sort_tmp_.alloc(tmp);
+        CK(cub::DeviceRadixSort::SortPairs(sort_tmp_.p, tmp, a_.p, keys32_.p, order_.p, order_.p + n_,
+                                           static_cast<int>(n_), 0, bits, stream_));
+        ++launches_;
+        return order_.p + n_;
+    }
+
+    // Column-tile width: the widest of 128 / 64 / 32 whose d × W fp32 slice
+    // fits the L2 budget (SSKM_TILE_BYTES, default 64 MiB of the 126 MB L2).
+    int tile_v() const {
+        const uint64_t budget = tile_bytes_;
+        for (int v : {4, 2, 1})
+            if (static_cast<uint64_t>(d_) * 32 * v * 4 <= budget) return v;
+        return 1;
     }
 
     template <int INIT>
-    void launch_scan(const AssignArgs& p, uint32_t ncols) {
-        const unsigned grid = grid_for(p.n_work * 32, 256);
-        if (ncols > 64 || INIT == kInitFull || INIT == kInitRescan) {
-            launch(assign_kernel<4, INIT>, grid, 256, p);
-        } else if (ncols > 32) {
-            launch(assign_kernel<2, INIT>, grid, 256, p);
-        } else {
-            launch(assign_kernel<1, INIT>, grid, 256, p);
+    void scan_tiles(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* order,
+                    int64_t n_work) {
+        int v = tile_v();
+        while (v > 1 && ncols <= static_cast<uint32_t>(16 * v)) v >>= 1;  // narrow lists: narrow tiles
+        const uint32_t W = 32u * v;
+        TileArgs p{};
+        p.indptr = indptr_.p;
+        p.idx = idx_.p;
+        p.val = val_.p;
+        p.M = M;
+        p.ld = ld;
+        p.ncols = ncols;
+        p.col_ids = col_ids;
+        p.order = order;
+        p.n_work = n_work;
+        p.a = a_.p;
+        p.sims = sims_.p;
+        p.unchanged = unchanged_.p;
+        p.a_start = a_start_.p;
+        p.sims_start = sims_start_.p;
+        p.CT = ct_.p;
+        p.ld_ct = ld_;
+        p.rescan_list = rescan_.p;
+        p.n_rescan = &scal_.p->n_rescan;
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+            1, std::min<int64_t>(static_cast<int64_t>(sms_) * blocks_per_sm_, ceil_div(n_work, 8))));
+        for (uint32_t c0 = 0; c0 < ncols; c0 += W) {
+            p.col0 = c0;
+            p.first = c0 == 0;
+            p.last = c0 + W >= ncols;
+            launch_tile<INIT>(v, grid, p);
         }
         CK_LAUNCH();
+    }
+
+    void screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
+                    const uint32_t* order, int64_t n_work) {
+        if (screen_kind_ == 1)
+            postings_screen(M, ld, ncols, col_ids, skip, order, n_work);
+        else
+            screen_tiles(M, ld, ncols, col_ids, skip, order, n_work);
+    }
+
+    // Inverted-index screen, one cluster tile at a time: build the tile's
+    // postings from the dense columns, then run the warp-per-document screen.
+    void postings_screen(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
+                         const uint32_t* order, int64_t n_work) {
+        sb_.alloc(n_);
+        ss_.alloc(n_);
+        sa_.alloc(n_);
+        pcnt_.alloc(d_ + 1);
+        pptr_.alloc(d_ + 1);
+        const uint32_t KT = ncols <= 256 ? 256 : (ncols <= 1024 ? 1024 : 2048);
+        PostingsArgs p{};
+        p.indptr = indptr_.p;
+        p.idx = idx_.p;
+        p.val = val_.p;
+        p.col_ids = col_ids;
+        p.order = order;
+        p.n_work = n_work;
+        p.skip_id = skip;
+        p.sb = sb_.p;
+        p.ss = ss_.p;
+        p.sa = sa_.p;
+        for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
+            const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
+            // postings of columns [c0, c0 + kt)
+            CK(cudaMemsetAsync(pcnt_.p + d_, 0, 8, stream_));
+            launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt,
+                   pcnt_.p);
+            size_t tmp = 0;
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
+            scan_tmp_.alloc(tmp);
+            CK(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
+            ++launches_;
+            int64_t total = 0;
+            CK(cudaMemcpyAsync(&total, pptr_.p + d_, 8, cudaMemcpyDeviceToHost, stream_));
+            CK(cudaStreamSynchronize(stream_));
+            pairs_.alloc(static_cast<size_t>(std::max<int64_t>(total, 1)));
+            launch(postings_fill_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt,
+                   pptr_.p, pairs_.p);
+            p.pptr = pptr_.p;
+            p.pairs = pairs_.p;
+            p.c0 = c0;
+            p.kt = kt;
+            p.first = c0 == 0;
+            postings_total_ += total;
+            if (KT == 256)
+                postings_launch<256>(p, n_work);
+            else if (KT == 1024)
+                postings_launch<1024>(p, n_work);
+            else
+                postings_launch<2048>(p, n_work);
+        }
+        CK_LAUNCH();
+    }
+
+    template <int KT>
+    void postings_launch(const PostingsArgs& p, int64_t n_work) {
+        auto k = postings_screen_kernel<KT>;
+        const size_t smem = static_cast<size_t>(8) * KT * sizeof(float);
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem));
+        per_sm = std::max(1, per_sm);
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(n_work, 8))));
+        k<<<grid, 256, smem, stream_>>>(p);
+        ++launches_;
+    }
+
+    void screen_tiles(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
+                      const uint32_t* order, int64_t n_work) {
+        sb_.alloc(n_);
+        ss_.alloc(n_);
+        sa_.alloc(n_);
+        int v = tile_v();
+        while (v > 1 && ncols <= static_cast<uint32_t>(16 * v)) v >>= 1;
+        const uint32_t W = 32u * v;
+        ScreenArgs p{};
+        p.indptr = indptr_.p;
+        p.idx = idx_.p;
+        p.val = val_.p;
+        p.M = M;
+        p.ld = ld;
+        p.ncols = ncols;
+        p.col_ids = col_ids;
+        p.order = order;
+        p.n_work = n_work;
+        p.skip_id = skip;
+        p.sb = sb_.p;
+        p.ss = ss_.p;
+        p.sa = sa_.p;
+        for (uint32_t c0 = 0; c0 < ncols; c0 += W) {
+            p.col0 = c0;
+            p.first = c0 == 0;
+            if (v == 4)
+                screen_launch<4>(p, n_work);
+            else if (v == 2)
+                screen_launch<2>(p, n_work);
+            else
+                screen_launch<1>(p, n_work);
+        }
+        CK_LAUNCH();
+    }
+
+    // One resident wave: blocks = SMs × occupancy, each a contiguous chunk of
+    // the cluster-ordered work list.
+    template <class K>
+    unsigned resident_grid(K kernel, int64_t n_work) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
+        per_sm = std::max(1, std::min(per_sm, screen_blocks_per_sm_));
+        return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm,
+                                                                            ceil_div(n_work, 8))));
+    }
+
+    template <int V>
+    void screen_launch(const ScreenArgs& p, int64_t n_work) {
+        if (screen_unroll_ >= 16) {
+            auto k = screen_tile_kernel<V, 16>;
+            launch(k, resident_grid(k, n_work), 256, p);
+        } else {
+            auto k = screen_tile_kernel<V, 8>;
+            launch(k, resident_grid(k, n_work), 256, p);
+        }
+    }
+
+    template <int INIT>
+    void resolve(const uint32_t* order, int64_t n_work) {
+        exact_.alloc(n_);
+        ResolveArgs r{};
+        r.indptr = indptr_.p;
+        r.idx = idx_.p;
+        r.val = val_.p;
+        r.CT = ct_.p;
+        r.ld_ct = ld_;
+        r.order = order;
+        r.n_work = n_work;
+        r.cmax = cmax_;
+        r.sb = sb_.p;
+        r.ss = ss_.p;
+        r.sa = sa_.p;
+        r.unchanged = unchanged_.p;
+        r.a_start = a_start_.p;
+        r.sims_start = sims_start_.p;
+        r.a = a_.p;
+        r.sims = sims_.p;
+        r.exact_list = exact_.p;
+        r.n_exact = &scal_.p->n_exact;
+        r.rescan_list = rescan_.p;
+        r.n_rescan = &scal_.p->n_rescan;
+        launch(resolve_kernel<INIT>, grid_for(n_work * 32, 256), 256, r);
+        CK_LAUNCH();
+    }
+
+    template <int INIT, int U>
+    void launch_tile_u(int v, unsigned grid, const TileArgs& p) {
+        if (v == 4)
+            launch(assign_tile_kernel<4, INIT, U>, grid, 256, p);
+        else if (v == 2)
+            launch(assign_tile_kernel<2, INIT, U>, grid, 256, p);
+        else
+            launch(assign_tile_kernel<1, INIT, U>, grid, 256, p);
+    }
+
+    template <int INIT>
+    void launch_tile(int v, unsigned grid, const TileArgs& p) {
+        if (unroll_ >= 16)
+            launch_tile_u<INIT, 16>(v, grid, p);
+        else if (unroll_ >= 8)
+            launch_tile_u<INIT, 8>(v, grid, p);
+        else
+            launch_tile_u<INIT, 4>(v, grid, p);
     }
 
     void finish_assign(sskm_iteration_stats* st) {
@@ -809,6 +1133,14 @@ private:
     static constexpr int kUserEvents = 16;
     cudaEvent_t user_ev_[kUserEvents]{};
     uint64_t launches_ = 0;
+    uint64_t tile_bytes_ = 64ull << 20;
+    bool order_enabled_ = true;
+    int blocks_per_sm_ = 2;
+    int unroll_ = 16;
+    int screen_blocks_per_sm_ = 8;
+    int screen_unroll_ = 16;
+    bool screen_enabled_ = true;
+    double cmax_ = 1.0;
     DevBuf<Scalars> scal_;
     Scalars* hs_ = nullptr;
 
@@ -830,9 +1162,20 @@ private:
     DevBuf<float> ct_, cc_;
     DevBuf<long long> S_;
     DevBuf<uint32_t> a_, a_sum_, a_start_, moved_, rescan_, rec_ids_, rec_pos_, chg_ids_;
+    DevBuf<double> sims_start_;
+    DevBuf<float> sb_, ss_;
+    DevBuf<int64_t> pcnt_, pptr_;
+    DevBuf<uint2> pairs_;
+    DevBuf<unsigned char> scan_tmp_;
+    int64_t postings_total_ = 0;
+    int screen_kind_ = 1;
+    DevBuf<uint32_t> sa_, exact_;
+    DevBuf<uint32_t> order_, keys32_;
     DevBuf<double> sims_, drift_, norm2_, drift_rec_, part_, obj_part_;
     DevBuf<uint8_t> unchanged_, touched_, repaired_flag_;
-    DevBuf<unsigned long long> counts_;
+    DevBuf<unsigned long long> counts_, keys_;
+    DevBuf<uint32_t> vals_;
+    DevBuf<unsigned char> sort_tmp_;
 };
 
 }  // namespace sskm_b200

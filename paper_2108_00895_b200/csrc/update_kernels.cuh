@@ -198,8 +198,10 @@ __global__ void reduce_partials_kernel(const double* __restrict__ part, uint32_t
     out[c] = s;
 }
 
-// Rewrite recomputed columns: c = S / ||S|| (fp64 division, then fp32), with
-// the squared drift against the previous fp32 column as fixed-order partials.
+// Rewrite recomputed columns: c = S · (1/||S||) in fp64, stored fp32, with the
+// squared drift against the previous fp32 column as fixed-order partials. (The
+// reference divides by the norm and iterates to a fixpoint, sparse_vector.cpp:
+// 160-209; both land within one fp64 ulp, below fp32 resolution.)
 __global__ void write_cols_kernel(const long long* __restrict__ S, float* __restrict__ CT,
                                   uint64_t ld, uint32_t d, const uint32_t* __restrict__ ids,
                                   uint32_t n_ids, const double* __restrict__ norm2,
@@ -213,16 +215,41 @@ __global__ void write_cols_kernel(const long long* __restrict__ S, float* __rest
         if (rb == 0) atomicOr(zero_flag, 1u);
         return;
     }
+    const double inv = 1.0 / nrm;
     const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
     double dr = 0.0;
+#pragma unroll 4
     for (uint32_t t = t0; t < t1; ++t) {
         const uint64_t o = static_cast<uint64_t>(t) * ld + j;
-        const float cn = static_cast<float>(static_cast<double>(S[o]) / nrm);
-        const double diff = static_cast<double>(cn) - static_cast<double>(CT[o]);
+        const long long q = S[o];
+        const float old = CT[o];
+        const float cn = q == 0 ? 0.f : static_cast<float>(static_cast<double>(q) * inv);
+        const double diff = static_cast<double>(cn) - static_cast<double>(old);
         dr = fma(diff, diff, dr);
-        CT[o] = cn;
+        if (cn != old) CT[o] = cn;
     }
     part[static_cast<uint64_t>(rb) * n_ids + c] = dr;
+}
+
+// Repair candidates: (orderable(sim), doc) keys for one stable radix sort.
+__global__ void sim_keys_kernel(const double* __restrict__ sims, int64_t n,
+                                unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        keys[i] = orderable(sims[i] + 0.0);  // +0.0 folds -0.0: the reference compares with <, where -0 == +0
+        vals[i] = static_cast<uint32_t>(i);
+    }
+}
+
+__global__ void gather_assign_kernel(const uint32_t* __restrict__ docs, uint32_t m,
+                                     const uint32_t* __restrict__ a, uint32_t* __restrict__ out) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < m; c += gridDim.x * blockDim.x)
+        out[c] = a[docs[c]];
+}
+
+__global__ void apply_moves_kernel(const uint32_t* __restrict__ pairs, uint32_t m, uint32_t* __restrict__ a) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < m; c += gridDim.x * blockDim.x)
+        a[pairs[2 * c]] = pairs[2 * c + 1];
 }
 
 // unchanged flags (detect_unchanged + repaired-forces-changed + iteration-1
@@ -279,6 +306,18 @@ __global__ void scatter_seeds_kernel(const int64_t* __restrict__ indptr, const i
         const uint32_t s = seeds[j];
         for (int64_t e = indptr[s] + lane; e < indptr[s + 1]; e += kWarp)
             CT[static_cast<uint64_t>(idx[e]) * ld + j] = val[e];
+    }
+}
+
+// max 2-norm of the seed rows (bound on the seed centroids' norms for the screen)
+__global__ void seed_norm_max_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ val,
+                                     const uint32_t* __restrict__ seeds, uint32_t k,
+                                     unsigned long long* max_bits) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+        const uint32_t s = seeds[j];
+        double q = 0.0;
+        for (int64_t e = indptr[s]; e < indptr[s + 1]; ++e) q = fma((double)val[e], (double)val[e], q);
+        atomicMax(max_bits, static_cast<unsigned long long>(__double_as_longlong(sqrt(q))));
     }
 }
 
