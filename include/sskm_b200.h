@@ -76,7 +76,10 @@ typedef struct {
     uint64_t n_exact;         /* documents the fp32 screen could not certify (exact fp64 scan) */
     double update_ms;         /* device time of compute_centroids + detect_unchanged */
     double assign_ms;         /* device time of the assignment step */
-    double assign_kernel_ms;  /* device time of the dominant assign kernel(s) only */
+    double assign_kernel_ms;  /* device time of the assign kernels (screen, resolve, exact) */
+    double screen_ms;         /* device time of the postings-screen kernel launches only */
+    uint32_t screen_launches; /* postings-screen launches in this assign (one per cluster tile) */
+    uint32_t reserved0;
 } sskm_iteration_stats;
 
 typedef struct sskm_ctx sskm_ctx;
@@ -146,6 +149,10 @@ int sskm_timer_record(sskm_ctx* ctx, int32_t slot);
 int sskm_timer_elapsed(sskm_ctx* ctx, int32_t a, int32_t b, double* ms);
 int sskm_launch_count(sskm_ctx* ctx, uint64_t* n);
 int sskm_synchronize(sskm_ctx* ctx);
+/* Σ over document nonzeros of the number of centroids with a nonzero weight on
+ * that term, for the current centroids: the (cluster, value) pairs one
+ * postings-screen assign streams (the kernel's algorithmic work). */
+int sskm_postings_work(sskm_ctx* ctx, uint64_t* pairs);
 
 /* One-shot drop-in for sskm::run(const CorpusMatrix&, const RunConfig&)
  * (engine.hpp:148): upload, seed (given seeds, or k-means++ when seeds is

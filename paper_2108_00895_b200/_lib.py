@@ -56,6 +56,9 @@ class sskm_iteration_stats(C.Structure):
         ("update_ms", C.c_double),
         ("assign_ms", C.c_double),
         ("assign_kernel_ms", C.c_double),
+        ("screen_ms", C.c_double),
+        ("screen_launches", C.c_uint32),
+        ("reserved0", C.c_uint32),
     ]
 
 
@@ -103,6 +106,7 @@ SIGNATURES = [
     ("sskm_timer_elapsed", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
     ("sskm_launch_count", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("sskm_synchronize", C.c_int, [_P]),
+    ("sskm_postings_work", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     # extension (not in the reference): teacher-forcing of the NCC flags
     ("sskm_set_unchanged", C.c_int, [_P, _u8p]),
     # synthetic corpus generator (csrc/synth.cpp)

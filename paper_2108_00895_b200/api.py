@@ -115,6 +115,9 @@ class IterationStats:
     update_ms: float = 0.0
     assign_ms: float = 0.0
     assign_kernel_ms: float = 0.0
+    screen_ms: float = 0.0
+    screen_launches: int = 0
+    reserved0: int = 0
 
     @classmethod
     def from_c(cls, s: sskm_iteration_stats) -> "IterationStats":
@@ -290,6 +293,11 @@ class Engine:
     def launch_count(self) -> int:
         n = C.c_uint64()
         check(self.lib.sskm_launch_count(self.h, C.byref(n)))
+        return int(n.value)
+
+    def postings_work(self) -> int:
+        n = C.c_uint64()
+        check(self.lib.sskm_postings_work(self.h, C.byref(n)))
         return int(n.value)
 
     def synchronize(self):

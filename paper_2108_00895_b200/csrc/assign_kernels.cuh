@@ -434,7 +434,7 @@ struct PostingsArgs {
     const int64_t* indptr;
     const int32_t* idx;
     const float* val;
-    const int64_t* pptr;       // d + 1 offsets into pairs for this cluster tile
+    const uint32_t* pptr;      // d + 1 offsets into pairs for this cluster tile (< 2^32)
     const uint2* pairs;        // (local cluster, float bits)
     uint32_t c0;               // first column of the tile (in M's column space)
     uint32_t kt;               // columns in this tile
@@ -448,7 +448,13 @@ struct PostingsArgs {
     uint32_t* sa;
 };
 
-template <int KT>
+__device__ __forceinline__ uint2 ld_pair(const uint2* p, uint64_t pol) {
+    uint2 pr;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(pr.x), "=r"(pr.y) : "l"(p), "l"(pol));
+    return pr;
+}
+
+template <int KT, int U>
 __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
     extern __shared__ float smem_acc[];
     const int lane = threadIdx.x & (kWarp - 1);
@@ -468,7 +474,7 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
         __syncwarp();
         for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
             const int64_t e = e0 + lane;
-            int64_t lb = 0, le = 0;
+            uint32_t lb = 0, le = 0;
             float x_l = 0.f;
             if (e < end) {
                 const int32_t t = ld_stream_i32(p.idx + e, pol_stream);
@@ -478,13 +484,11 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
             }
             const int n = static_cast<int>(imin64(kWarp, end - e0));
             for (int j = 0; j < n; ++j) {
-                const int64_t b = __shfl_sync(0xFFFFFFFFu, lb, j);
-                const int64_t en = __shfl_sync(0xFFFFFFFFu, le, j);
+                const uint32_t qb = __shfl_sync(0xFFFFFFFFu, lb, j);
+                const uint32_t qe = __shfl_sync(0xFFFFFFFFu, le, j);
                 const float x = __shfl_sync(0xFFFFFFFFu, x_l, j);
-                for (int64_t q = b + lane; q < en; q += kWarp) {
-                    uint2 pr;
-                    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
-                                 : "=r"(pr.x), "=r"(pr.y) : "l"(p.pairs + q), "l"(pol_keep));
+                for (uint32_t q = qb + lane; q < qe; q += kWarp) {
+                    const uint2 pr = ld_pair(p.pairs + q, pol_keep);
                     acc[pr.x] = fmaf(x, __uint_as_float(pr.y), acc[pr.x]);
                 }
                 __syncwarp();
@@ -519,10 +523,21 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
     }
 }
 
+__global__ void postings_work_kernel(const int32_t* __restrict__ idx, int64_t nnz, const uint32_t* __restrict__ cnt,
+                                     unsigned long long* total) {
+    unsigned long long s = 0;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        s += cnt[idx[e]];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
+    if ((threadIdx.x & 31) == 0) atomicAdd(total, s);
+}
+
 // Postings build from the dense column tile [c0, c0 + kt) of M: per-row counts,
 // then (after an exclusive scan) the pairs in ascending cluster order.
 __global__ void postings_count_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d, uint32_t c0,
-                                      uint32_t kt, int64_t* __restrict__ cnt) {
+                                      uint32_t kt, uint32_t* __restrict__ cnt) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
@@ -537,13 +552,13 @@ __global__ void postings_count_kernel(const float* __restrict__ M, uint64_t ld, 
 }
 
 __global__ void postings_fill_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d, uint32_t c0,
-                                     uint32_t kt, const int64_t* __restrict__ pptr, uint2* __restrict__ pairs) {
+                                     uint32_t kt, const uint32_t* __restrict__ pptr, uint2* __restrict__ pairs) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
     for (uint64_t t = gw; t < d; t += nw) {
         const float* row = M + t * ld + c0;
-        int64_t pos = pptr[t];
+        uint32_t pos = pptr[t];
         for (uint32_t j0 = 0; j0 < kt; j0 += kWarp) {
             const uint32_t j = j0 + lane;
             const float v = j < kt ? row[j] : 0.f;
@@ -620,9 +635,11 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
                 certain = best > -2.0;
             }
         } else {
-            const uint32_t a0 = p.a_start[i];
-            old_sim = p.sims_start[i];
-            own_changed = p.unchanged[a0] == 0;
+            // NCC pass A: cached or refreshed own similarity (engine.cpp:268-273);
+            // rescan pass: the exact running best from pass A
+            const uint32_t a0 = INIT == kInitRescan ? p.a[i] : p.a_start[i];
+            old_sim = INIT == kInitRescan ? p.sims[i] : p.sims_start[i];
+            own_changed = INIT == kInitNcc && p.unchanged[a0] == 0;
             const double sim0 = own_changed ? doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, a0, lane)
                                             : old_sim;
             best = sim0;
@@ -660,6 +677,22 @@ __global__ void iota_kernel(uint32_t* __restrict__ p, int64_t n) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         p[i] = static_cast<uint32_t>(i);
+}
+
+// NCC dot accounting when the exact full scan replaced the changed-list scan
+// (ncc_epsilon = 0): unchanged centroids keep bit-identical similarities, all
+// <= the cached max, so "the refreshed changed scan did not beat the cache"
+// (engine.cpp:303) is exactly !(final best > cached sim) for a changed-own doc.
+__global__ void ncc_rescan_count_kernel(const uint32_t* __restrict__ a_start, const double* __restrict__ sims_start,
+                                        const double* __restrict__ sims, const uint8_t* __restrict__ unchanged,
+                                        int64_t n, unsigned long long* n_rescan) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        c += unchanged[a_start[i]] == 0 && !(sims[i] > sims_start[i]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, off);
+    if ((threadIdx.x & 31) == 0) atomicAdd(n_rescan, c);
 }
 
 // Σ sims (fixed-shape tree: bitwise reproducible for a given n) and the

@@ -82,6 +82,8 @@ public:
         if (const char* e = std::getenv("SSKM_ORDER")) order_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_UNROLL")) unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_SCREEN_UNROLL")) screen_unroll_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
+        if (const char* e = std::getenv("SSKM_POST_UNROLL")) post_unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_SCREEN_KIND")) screen_kind_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_SCREEN")) screen_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SCREEN_BLOCKS_PER_SM")) screen_blocks_per_sm_ = std::max(1, std::atoi(e));
@@ -228,6 +230,7 @@ public:
         }
         if (cfg_.mode != SSKM_MODE_BASELINE) cc_.alloc(static_cast<uint64_t>(d_) * ld_);
         obj_part_.alloc(kObjBlocks);
+        prealloc();
     }
 
     // -------------------------------------------------------------- init --
@@ -427,6 +430,7 @@ public:
         }
         CK(cudaEventRecord(ev_[5], stream_));
         finish_assign(st);
+        cache_trusted_ = true;
         st->n_unchanged_centroids = iteration_ <= 1 ? 0 : n_unchanged_;
         st->dot_products = static_cast<uint64_t>(k_) * static_cast<uint64_t>(n_);
         st->gpu_dot_products = st->dot_products + n_exact * k_;
@@ -443,8 +447,25 @@ public:
         const uint32_t* order = cluster_order();
         reset_scalars();
         CK(cudaEventRecord(ev_[4], stream_));
-        uint64_t n_exact = 0;
-        if (n_chg_ > 0) {
+        uint64_t n_exact = 0, n_rescan = 0;
+        // With ncc_epsilon = 0 and a cache this engine produced, the NCC result
+        // equals the full scan bit for bit; when many centroids
+        // changed the full screened scan is the cheaper way to get it.
+        const bool full_equiv = cfg_.ncc_epsilon == 0.0 && cache_trusted_ && screen_enabled_ &&
+                                static_cast<double>(n_chg_) >= ncc_full_frac_ * k_;
+        if (n_chg_ > 0 && full_equiv) {
+            screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_);
+            resolve<kInitFull>(order, n_);
+            pull_scalars();
+            n_exact = hs_->n_exact;
+            if (n_exact > 0) scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(n_exact));
+            CK(cudaMemsetAsync(&scal_.p->n_rescan, 0, 8, stream_));
+            launch(ncc_rescan_count_kernel, grid_for(n_, 256), 256, a_start_.p, sims_start_.p, sims_.p, unchanged_.p,
+                   n_, &scal_.p->n_rescan);
+            CK_LAUNCH();
+            pull_scalars();
+            n_rescan = hs_->n_rescan;
+        } else if (n_chg_ > 0) {
             if (screen_enabled_) {
                 screen_any(cc_.p, ld_cc_, n_chg_, chg_ids_.p, a_start_.p, order, n_);
                 resolve<kInitNcc>(order, n_);
@@ -455,12 +476,26 @@ public:
             } else {
                 scan_tiles<kInitNcc>(cc_.p, ld_cc_, n_chg_, chg_ids_.p, order, n_);
             }
+            pull_scalars();
+            n_rescan = hs_->n_rescan;
+            if (n_rescan > 0) {
+                // pass B over all centroids for the rescan documents (engine.cpp:303-305)
+                if (screen_enabled_) {
+                    CK(cudaMemsetAsync(&scal_.p->n_exact, 0, 8, stream_));
+                    screen_any(ct_.p, ld_, k_, nullptr, a_.p, rescan_.p, static_cast<int64_t>(n_rescan));
+                    resolve<kInitRescan>(rescan_.p, static_cast<int64_t>(n_rescan));
+                    pull_scalars();
+                    const uint64_t nx = hs_->n_exact;
+                    n_exact += nx;
+                    if (nx > 0) scan_tiles<kInitRescan>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(nx));
+                } else {
+                    scan_tiles<kInitRescan>(ct_.p, ld_, k_, nullptr, rescan_.p, static_cast<int64_t>(n_rescan));
+                }
+            }
         }
-        pull_scalars();
-        const uint64_t n_rescan = hs_->n_rescan;
-        if (n_rescan > 0) scan_tiles<kInitRescan>(ct_.p, ld_, k_, nullptr, rescan_.p, static_cast<int64_t>(n_rescan));
         CK(cudaEventRecord(ev_[5], stream_));
         finish_assign(st);
+        cache_trusted_ = true;
         // dot accounting of the reference (engine.cpp:253-306): every document
         // evaluates the changed list (minus its own centroid, which a
         // changed-own document evaluates as its refresh), plus the unchanged
@@ -468,7 +503,8 @@ public:
         const uint64_t n_unch = k_ - n_chg_;
         st->n_unchanged_centroids = static_cast<uint32_t>(n_unch);
         st->dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_rescan * n_unch;
-        st->gpu_dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_exact * n_chg_ + n_rescan * k_;
+        st->gpu_dot_products = full_equiv ? static_cast<uint64_t>(n_) * k_
+                                          : static_cast<uint64_t>(n_) * n_chg_ + n_rescan * k_;
         st->n_changed = n_chg_;
         st->n_rescan = n_rescan;
         st->n_exact = n_exact;
@@ -499,6 +535,7 @@ public:
         }
         if (sims) CK(cudaMemcpyAsync(sims_.p, sims, n_ * 8, cudaMemcpyHostToDevice, stream_));
         iteration_ = iteration;
+        cache_trusted_ = false;  // externally supplied cache: follow the reference's NCC literally
         CK(cudaStreamSynchronize(stream_));
     }
 
@@ -527,6 +564,7 @@ public:
         for (double q : nrm) cmax_ = std::max(cmax_, std::sqrt(q) * (1.0 + 1e-12));
         reset_sums();
         have_cc_ = false;
+        cache_trusted_ = false;
         CK(cudaStreamSynchronize(stream_));
     }
 
@@ -534,6 +572,7 @@ public:
         need_state();
         CK(cudaMemcpyAsync(unchanged_.p, flags, k_, cudaMemcpyHostToDevice, stream_));
         have_cc_ = false;
+        cache_trusted_ = false;
         CK(cudaStreamSynchronize(stream_));
     }
 
@@ -654,6 +693,32 @@ private:
         CK(cudaStreamSynchronize(stream_));
     }
 
+    // All per-iteration scratch is sized once here, so no cudaMalloc (and its
+    // implicit device synchronisation) ever runs inside an iteration.
+    void prealloc() {
+        keys_.alloc(2 * n_);
+        vals_.alloc(2 * n_);
+        order_.alloc(2 * n_);
+        keys32_.alloc(n_);
+        sb_.alloc(n_);
+        ss_.alloc(n_);
+        sa_.alloc(n_);
+        exact_.alloc(n_);
+        pcnt_.alloc(d_ + 1);
+        pptr_.alloc(d_ + 1);
+        moves_.alloc(2 * static_cast<size_t>(k_));
+        size_t t1 = 0, t2 = 0, t3 = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys_.p, keys_.p + n_, vals_.p, vals_.p + n_,
+                                           static_cast<int>(n_), 0, 64, stream_));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, t2, a_.p, keys32_.p, order_.p, order_.p + n_,
+                                           static_cast<int>(n_), 0, 32, stream_));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, t3, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
+        sort_tmp_.alloc(std::max(t1, t2));
+        scan_tmp_.alloc(t3);
+        // postings: start at 10% density of a 2048-cluster tile, grow by 1.5x
+        pairs_.alloc(std::max<size_t>(1, static_cast<size_t>(d_) * std::min<uint32_t>(ld_, 2048) / 10));
+    }
+
     // Bound on the centroid column norms after a seed init (the screen's δ).
     void seed_cmax(const uint32_t* dseeds) {
         reset_scalars();
@@ -758,10 +823,8 @@ private:
             repaired_.push_back(moves[q + 1]);
             flag[moves[q + 1]] = 1;
         }
-        DevBuf<uint32_t> dm;
-        dm.alloc(moves.size());
-        CK(cudaMemcpyAsync(dm.p, moves.data(), moves.size() * 4, cudaMemcpyHostToDevice, stream_));
-        launch(apply_moves_kernel, 1, 256, dm.p, static_cast<uint32_t>(moves.size() / 2), a_.p);
+        CK(cudaMemcpyAsync(moves_.p, moves.data(), moves.size() * 4, cudaMemcpyHostToDevice, stream_));
+        launch(apply_moves_kernel, 1, 256, moves_.p, static_cast<uint32_t>(moves.size() / 2), a_.p);
         CK_LAUNCH();
         CK(cudaMemcpyAsync(repaired_flag_.p, flag.data(), k_, cudaMemcpyHostToDevice, stream_));
         CK(cudaStreamSynchronize(stream_));
@@ -850,6 +913,8 @@ private:
     }
 
     void snapshot_start() {
+        screen_ms_ = 0.0;
+        screen_launches_ = 0;
         CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
         CK(cudaMemcpyAsync(sims_start_.p, sims_.p, n_ * 8, cudaMemcpyDeviceToDevice, stream_));
     }
@@ -937,7 +1002,9 @@ private:
         sa_.alloc(n_);
         pcnt_.alloc(d_ + 1);
         pptr_.alloc(d_ + 1);
+        // tile pairs are addressed with 32-bit offsets: d · KT < 2^32
         const uint32_t KT = ncols <= 256 ? 256 : (ncols <= 1024 ? 1024 : 2048);
+        if (static_cast<uint64_t>(d_) * KT >= (1ull << 32)) throw InvalidArgument("vocabulary too large for postings");
         PostingsArgs p{};
         p.indptr = indptr_.p;
         p.idx = idx_.p;
@@ -952,7 +1019,7 @@ private:
         for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
             const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
             // postings of columns [c0, c0 + kt)
-            CK(cudaMemsetAsync(pcnt_.p + d_, 0, 8, stream_));
+            CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
             launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt,
                    pcnt_.p);
             size_t tmp = 0;
@@ -960,10 +1027,10 @@ private:
             scan_tmp_.alloc(tmp);
             CK(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
             ++launches_;
-            int64_t total = 0;
-            CK(cudaMemcpyAsync(&total, pptr_.p + d_, 8, cudaMemcpyDeviceToHost, stream_));
+            uint32_t total = 0;
+            CK(cudaMemcpyAsync(&total, pptr_.p + d_, 4, cudaMemcpyDeviceToHost, stream_));
             CK(cudaStreamSynchronize(stream_));
-            pairs_.alloc(static_cast<size_t>(std::max<int64_t>(total, 1)));
+            if (total > pairs_.n) pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
             launch(postings_fill_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt,
                    pptr_.p, pairs_.p);
             p.pptr = pptr_.p;
@@ -972,19 +1039,57 @@ private:
             p.kt = kt;
             p.first = c0 == 0;
             postings_total_ += total;
+            CK(cudaEventRecord(ev_[6], stream_));
             if (KT == 256)
                 postings_launch<256>(p, n_work);
             else if (KT == 1024)
                 postings_launch<1024>(p, n_work);
             else
                 postings_launch<2048>(p, n_work);
+            CK(cudaEventRecord(ev_[7], stream_));
+            CK(cudaEventSynchronize(ev_[7]));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
+            screen_ms_ += ms;
+            screen_launches_ += 1;
         }
         CK_LAUNCH();
     }
 
+    // Σ over document nonzeros of the posting-list length of their term, for
+    // the last built tile set: the (cluster, value) pairs the screen streams.
+public:
+    uint64_t postings_work() {
+        need_state();
+        reset_scalars();
+        uint64_t total = 0;
+        const uint32_t KT = k_ <= 256 ? 256 : (k_ <= 1024 ? 1024 : 2048);
+        for (uint32_t c0 = 0; c0 < k_; c0 += KT) {
+            const uint32_t kt = std::min<uint32_t>(KT, k_ - c0);
+            CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
+            launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, ct_.p, (uint64_t)ld_, d_,
+                   c0, kt, pcnt_.p);
+            CK(cudaMemsetAsync(&scal_.p->n_moved, 0, 8, stream_));
+            launch(postings_work_kernel, grid_for(nnz_, 256), 256, idx_.p, nnz_, pcnt_.p, &scal_.p->n_moved);
+            CK_LAUNCH();
+            pull_scalars();
+            total += hs_->n_moved;
+        }
+        return total;
+    }
+
+private:
     template <int KT>
     void postings_launch(const PostingsArgs& p, int64_t n_work) {
-        auto k = postings_screen_kernel<KT>;
+        if (post_unroll_ >= 8)
+            postings_launch_u<KT, 8>(p, n_work);
+        else
+            postings_launch_u<KT, 4>(p, n_work);
+    }
+
+    template <int KT, int U>
+    void postings_launch_u(const PostingsArgs& p, int64_t n_work) {
+        auto k = postings_screen_kernel<KT, U>;
         const size_t smem = static_cast<size_t>(8) * KT * sizeof(float);
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
@@ -1124,6 +1229,8 @@ private:
         CK(cudaEventElapsedTime(&kms, ev_[4], ev_[5]));
         st->assign_ms = ms;
         st->assign_kernel_ms = kms;
+        st->screen_ms = screen_ms_;
+        st->screen_launches = screen_launches_;
     }
 
     int device_;
@@ -1164,17 +1271,22 @@ private:
     DevBuf<uint32_t> a_, a_sum_, a_start_, moved_, rescan_, rec_ids_, rec_pos_, chg_ids_;
     DevBuf<double> sims_start_;
     DevBuf<float> sb_, ss_;
-    DevBuf<int64_t> pcnt_, pptr_;
+    DevBuf<uint32_t> pcnt_, pptr_;
     DevBuf<uint2> pairs_;
     DevBuf<unsigned char> scan_tmp_;
     int64_t postings_total_ = 0;
+    double screen_ms_ = 0.0;
+    uint32_t screen_launches_ = 0;
     int screen_kind_ = 1;
+    int post_unroll_ = 8;
+    bool cache_trusted_ = false;
+    double ncc_full_frac_ = 0.25;
     DevBuf<uint32_t> sa_, exact_;
     DevBuf<uint32_t> order_, keys32_;
     DevBuf<double> sims_, drift_, norm2_, drift_rec_, part_, obj_part_;
     DevBuf<uint8_t> unchanged_, touched_, repaired_flag_;
     DevBuf<unsigned long long> counts_, keys_;
-    DevBuf<uint32_t> vals_;
+    DevBuf<uint32_t> vals_, moves_;
     DevBuf<unsigned char> sort_tmp_;
 };
 
@@ -1237,6 +1349,9 @@ void step(Engine& e, sskm_iteration_stats* st) {
     st->objective = a.objective;
     st->assign_ms = a.assign_ms;
     st->assign_kernel_ms = a.assign_kernel_ms;
+    st->screen_ms = a.screen_ms;
+    st->screen_launches = a.screen_launches;
+    st->n_exact = a.n_exact;
     st->index_active = 0;
     st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -1430,6 +1545,10 @@ int sskm_launch_count(sskm_ctx* ctx, uint64_t* n) {
 
 int sskm_synchronize(sskm_ctx* ctx) {
     return guard([&] { E(ctx).synchronize(); });
+}
+
+int sskm_postings_work(sskm_ctx* ctx, uint64_t* pairs) {
+    return guard([&] { *pairs = E(ctx).postings_work(); });
 }
 
 int sskm_local_sims_sum(sskm_ctx* ctx, double* sum) {

@@ -8,10 +8,8 @@ from paper_2108_00895_b200 import synthetic as S
 cfg = S.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c1"]
 data = S.corpus(cfg)
 seeds = S.init_seeds(data.n_docs, cfg.k, 0)
-variants = [dict(SSKM_SCREEN="0", SSKM_TILE_BYTES=str(128 << 20), SSKM_ORDER="1", SSKM_UNROLL="16"),
-            dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="0", SSKM_TILE_BYTES=str(128 << 20), SSKM_ORDER="0", SSKM_SCREEN_UNROLL="16"),
-            dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="1", SSKM_ORDER="0"),
-            dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="1", SSKM_ORDER="1")]
+variants = [dict(SSKM_SCREEN="0", SSKM_TILE_BYTES=str(128 << 20), SSKM_ORDER="1", SSKM_UNROLL="16")]
+variants += [dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="1", SSKM_ORDER=str(o), SSKM_POST_UNROLL=str(u)) for o in (0, 1) for u in (4, 8)]
 ref_a = None
 for v in variants:
     os.environ.update(v)
