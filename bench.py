@@ -212,7 +212,7 @@ def run_ours(args):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    if world > 1:
+    if world > 1 or args.distributed:
         from paper_2108_00895_b200 import distributed as D
 
         return D.bench_distributed(args)
@@ -317,6 +317,7 @@ def main():
     ap.add_argument("--mode", default="baseline", choices=["baseline", "ncc", "ncc+index"])
     ap.add_argument("--ref-sample", type=int, default=2000)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--distributed", action="store_true", help="use the sharded driver even at N=1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

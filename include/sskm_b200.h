@@ -171,15 +171,21 @@ int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims,
 
 /* Local cluster sizes (int64[k]) for the global empty-cluster check. */
 int sskm_local_counts(sskm_ctx* ctx, int64_t* counts);
-/* Lowest-(sim, global doc id) local donor among docs whose cluster has global
- * size >= 2 (engine.cpp:156-161). Writes sim and global id (INT64_MAX if none). */
-int sskm_local_donor(sskm_ctx* ctx, const int64_t* global_counts, double* sim, int64_t* doc);
+/* The first m local documents in the reference's repair-donor order (lowest
+ * cached sim, then lowest index; engine.cpp:156-161): their sims, global ids
+ * and current clusters (host arrays). The driver merges all ranks' lists and
+ * replays the sequential repair rule identically on every rank. */
+int sskm_local_candidates(sskm_ctx* ctx, int64_t m, double* sims, int64_t* gids, uint32_t* clusters,
+                          int64_t* m_out);
 /* Reassign a local document (repair move, engine.cpp:162-165). */
 int sskm_move_doc(sskm_ctx* ctx, int64_t global_doc, uint32_t cluster);
-/* Packs the locally moved documents: header counts then payload, see DESIGN.md. */
-int sskm_moved_size(sskm_ctx* ctx, int64_t* n_moved, int64_t* nnz_moved);
-int sskm_moved_pack(sskm_ctx* ctx, int64_t* doc_ids, uint32_t* old_c, uint32_t* new_c,
-                    int64_t* row_ptr, int32_t* idx, float* val);
+/* Moved documents of this shard: count and total nonzeros (device-side). */
+int sskm_moved_prepare(sskm_ctx* ctx, int64_t* n_moved, int64_t* nnz_moved);
+/* Packs them into caller-owned DEVICE buffers: old/new cluster per document,
+ * row lengths, and the rows' indices and values back to back. */
+int sskm_moved_pack(sskm_ctx* ctx, uint32_t* old_c, uint32_t* new_c, int32_t* lens, int32_t* idx, float* val);
+/* Seed init from the k seed rows gathered across shards (host CSR, k rows). */
+int sskm_init_from_rows(sskm_ctx* ctx, const int64_t* row_ptr, const int32_t* idx, const float* val);
 /* Applies gathered moved rows (DEVICE pointers on this context's GPU; rows
  * from all ranks, any order) to the
  * replicated sums, then finishes the update exactly like sskm_update. */

@@ -96,10 +96,11 @@ SIGNATURES = [
                                    _ST, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_double)]),
     ("sskm_local_counts", C.c_int, [_P, _i64p]),
-    ("sskm_local_donor", C.c_int, [_P, _i64p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    ("sskm_local_candidates", C.c_int, [_P, C.c_int64, _f64p, _i64p, _u32p, C.POINTER(C.c_int64)]),
     ("sskm_move_doc", C.c_int, [_P, C.c_int64, C.c_uint32]),
-    ("sskm_moved_size", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
-    ("sskm_moved_pack", C.c_int, [_P, _i64p, _u32p, _u32p, _i64p, _i32p, _f32p]),
+    ("sskm_moved_prepare", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("sskm_moved_pack", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("sskm_init_from_rows", C.c_int, [_P, _i64p, _i32p, _f32p]),
     ("sskm_update_apply", C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _u32p, C.c_uint32, _ST]),
     ("sskm_local_sims_sum", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("sskm_timer_record", C.c_int, [_P, C.c_int32]),

@@ -591,22 +591,6 @@ public:
         CK(cudaStreamSynchronize(stream_));
     }
 
-    void local_donor(const int64_t* global_counts, double* sim, int64_t* doc) {
-        need_state();
-        CK(cudaMemcpyAsync(counts_.p, global_counts, k_ * 8, cudaMemcpyHostToDevice, stream_));
-        uint64_t idx = find_donor();
-        if (idx == ULLONG_MAX) {
-            *doc = INT64_MAX;
-            *sim = 0.0;
-            return;
-        }
-        double s;
-        CK(cudaMemcpyAsync(&s, sims_.p + idx, 8, cudaMemcpyDeviceToHost, stream_));
-        CK(cudaStreamSynchronize(stream_));
-        *sim = s;
-        *doc = static_cast<int64_t>(idx) + doc_offset_;
-    }
-
     void move_doc(int64_t global_doc, uint32_t cluster) {
         need_state();
         const int64_t i = global_doc - doc_offset_;
@@ -615,47 +599,98 @@ public:
         CK(cudaStreamSynchronize(stream_));
     }
 
-    void moved_size(int64_t* n_moved, int64_t* nnz_moved) {
+    // Locally moved documents (cluster differs from the one their row is
+    // summed into), their row lengths and packed-row offsets — on the device.
+    void moved_prepare(int64_t* n_moved, int64_t* nnz_moved) {
         need_state();
         reset_scalars();
         launch(moved_kernel, grid_for(n_, 256), 256, a_.p, a_sum_.p, n_, moved_.p, &scal_.p->n_moved);
+        mv_len_.alloc(n_ + 1);
+        mv_off_.alloc(n_ + 1);
+        mv_old_.alloc(n_);
+        mv_new_.alloc(n_);
+        launch(moved_meta_kernel, grid_for(n_ + 1, 256), 256, moved_.p, &scal_.p->n_moved, indptr_.p, a_.p, a_sum_.p,
+               mv_len_.p, mv_old_.p, mv_new_.p);
         CK_LAUNCH();
         pull_scalars();
-        const uint64_t m = hs_->n_moved;
-        moved_host_.resize(m);
-        if (m) CK(cudaMemcpyAsync(moved_host_.data(), moved_.p, m * 4, cudaMemcpyDeviceToHost, stream_));
-        CK(cudaStreamSynchronize(stream_));
-        std::sort(moved_host_.begin(), moved_host_.end());
-        ptr_host_.resize(n_ + 1);
-        CK(cudaMemcpy(ptr_host_.data(), indptr_.p, (n_ + 1) * 8, cudaMemcpyDeviceToHost));
+        mv_n_ = static_cast<int64_t>(hs_->n_moved);
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, mv_len_.p, mv_off_.p, static_cast<int>(mv_n_ + 1), stream_));
+        scan_tmp_.alloc(tmp);
+        CK(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, mv_len_.p, mv_off_.p, static_cast<int>(mv_n_ + 1), stream_));
+        ++launches_;
         int64_t nnz = 0;
-        for (uint32_t i : moved_host_) nnz += ptr_host_[i + 1] - ptr_host_[i];
-        *n_moved = static_cast<int64_t>(m);
+        CK(cudaMemcpyAsync(&nnz, mv_off_.p + mv_n_, 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        mv_nnz_ = nnz;
+        *n_moved = mv_n_;
         *nnz_moved = nnz;
     }
 
-    // Host-side packing of the local moved rows (ascending local doc order).
-    void moved_pack(int64_t* doc_ids, uint32_t* old_c, uint32_t* new_c, int64_t* row_ptr, int32_t* idx,
-                    float* val) {
+    // Packs the prepared rows into caller-owned DEVICE buffers.
+    void moved_pack(uint32_t* old_c, uint32_t* new_c, int32_t* lens, int32_t* idx, float* val) {
         need_state();
-        std::vector<uint32_t> a(n_), as(n_);
-        CK(cudaMemcpy(a.data(), a_.p, n_ * 4, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(as.data(), a_sum_.p, n_ * 4, cudaMemcpyDeviceToHost));
-        int64_t p = 0;
-        row_ptr[0] = 0;
-        for (size_t m = 0; m < moved_host_.size(); ++m) {
-            const uint32_t i = moved_host_[m];
-            doc_ids[m] = static_cast<int64_t>(i) + doc_offset_;
-            old_c[m] = as[i];
-            new_c[m] = a[i];
-            const int64_t b = ptr_host_[i], e = ptr_host_[i + 1];
-            if (e > b) {
-                CK(cudaMemcpy(idx + p, idx_.p + b, (e - b) * 4, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(val + p, val_.p + b, (e - b) * 4, cudaMemcpyDeviceToHost));
-            }
-            p += e - b;
-            row_ptr[m + 1] = p;
+        if (mv_n_ > 0) {
+            CK(cudaMemcpyAsync(old_c, mv_old_.p, mv_n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+            CK(cudaMemcpyAsync(new_c, mv_new_.p, mv_n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+            launch(pack_rows_kernel, grid_for(mv_n_ * 32, 256), 256, moved_.p, mv_n_, indptr_.p, idx_.p, val_.p,
+                   mv_off_.p, lens, idx, val);
+            CK_LAUNCH();
         }
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    // The first m local repair candidates in the reference's donor order
+    // (lowest cached sim, then lowest document index): sims, global ids and
+    // current clusters (host arrays).
+    int64_t local_candidates(int64_t m, double* sims, int64_t* gids, uint32_t* clusters) {
+        need_state();
+        m = std::min<int64_t>(m, n_);
+        sort_sim_candidates();
+        std::vector<uint32_t> docs(m), cur(m);
+        fetch_candidates(static_cast<uint64_t>(m), docs.data(), cur.data());
+        std::vector<double> all(n_);
+        CK(cudaMemcpyAsync(all.data(), sims_.p, n_ * 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        for (int64_t q = 0; q < m; ++q) {
+            sims[q] = all[docs[q]];
+            gids[q] = static_cast<int64_t>(docs[q]) + doc_offset_;
+            clusters[q] = cur[q];
+        }
+        return m;
+    }
+
+    // Multi-GPU seed init: centroid j = row j of a k-row CSR (host arrays) —
+    // the seed documents gathered from whichever shard owns them.
+    void init_from_rows(const int64_t* rptr, const int32_t* ridx, const float* rval) {
+        need_config();
+        const int64_t nnz = rptr[k_];
+        DevBuf<int64_t> dp;
+        DevBuf<int32_t> di;
+        DevBuf<float> dv;
+        dp.alloc(k_ + 1);
+        di.alloc(std::max<int64_t>(nnz, 1));
+        dv.alloc(std::max<int64_t>(nnz, 1));
+        CK(cudaMemcpyAsync(dp.p, rptr, (k_ + 1) * 8, cudaMemcpyHostToDevice, stream_));
+        if (nnz) {
+            CK(cudaMemcpyAsync(di.p, ridx, nnz * 4, cudaMemcpyHostToDevice, stream_));
+            CK(cudaMemcpyAsync(dv.p, rval, nnz * 4, cudaMemcpyHostToDevice, stream_));
+        }
+        CK(cudaMemsetAsync(ct_.p, 0, static_cast<uint64_t>(d_) * ld_ * sizeof(float), stream_));
+        launch(scatter_rows_kernel, grid_for(static_cast<int64_t>(k_) * 32, 256), 256, dp.p, di.p, dv.p, k_, ct_.p,
+               (uint64_t)ld_);
+        CK_LAUNCH();
+        double m = 0.0;
+        for (uint32_t j = 0; j < k_; ++j) {
+            double q = 0.0;
+            for (int64_t e = rptr[j]; e < rptr[j + 1]; ++e) q += static_cast<double>(rval[e]) * rval[e];
+            m = std::max(m, std::sqrt(q));
+        }
+        cmax_ = std::max(m, 1e-300) * (1.0 + 1e-12);
+        seed_assign_state();
+        sskm_iteration_stats st{};
+        full_assign(&st);
+        CK(cudaStreamSynchronize(stream_));
     }
 
     double local_sims_sum() {
@@ -1260,8 +1295,6 @@ private:
     sskm_run_config cfg_{};
     std::vector<double> lambdas_;
     std::vector<uint32_t> repaired_;
-    std::vector<uint32_t> moved_host_;
-    std::vector<int64_t> ptr_host_;
 
     DevBuf<int64_t> indptr_;
     DevBuf<int32_t> idx_;
@@ -1286,7 +1319,9 @@ private:
     DevBuf<double> sims_, drift_, norm2_, drift_rec_, part_, obj_part_;
     DevBuf<uint8_t> unchanged_, touched_, repaired_flag_;
     DevBuf<unsigned long long> counts_, keys_;
-    DevBuf<uint32_t> vals_, moves_;
+    DevBuf<uint32_t> vals_, moves_, mv_old_, mv_new_;
+    DevBuf<int64_t> mv_len_, mv_off_;
+    int64_t mv_n_ = 0, mv_nnz_ = 0;
     DevBuf<unsigned char> sort_tmp_;
 };
 
@@ -1508,21 +1543,25 @@ int sskm_local_counts(sskm_ctx* ctx, int64_t* counts) {
     return guard([&] { E(ctx).local_counts(counts); });
 }
 
-int sskm_local_donor(sskm_ctx* ctx, const int64_t* global_counts, double* sim, int64_t* doc) {
-    return guard([&] { E(ctx).local_donor(global_counts, sim, doc); });
-}
-
 int sskm_move_doc(sskm_ctx* ctx, int64_t global_doc, uint32_t cluster) {
     return guard([&] { E(ctx).move_doc(global_doc, cluster); });
 }
 
-int sskm_moved_size(sskm_ctx* ctx, int64_t* n_moved, int64_t* nnz_moved) {
-    return guard([&] { E(ctx).moved_size(n_moved, nnz_moved); });
+int sskm_moved_prepare(sskm_ctx* ctx, int64_t* n_moved, int64_t* nnz_moved) {
+    return guard([&] { E(ctx).moved_prepare(n_moved, nnz_moved); });
 }
 
-int sskm_moved_pack(sskm_ctx* ctx, int64_t* doc_ids, uint32_t* old_c, uint32_t* new_c, int64_t* row_ptr,
-                    int32_t* idx, float* val) {
-    return guard([&] { E(ctx).moved_pack(doc_ids, old_c, new_c, row_ptr, idx, val); });
+int sskm_moved_pack(sskm_ctx* ctx, uint32_t* old_c, uint32_t* new_c, int32_t* lens, int32_t* idx, float* val) {
+    return guard([&] { E(ctx).moved_pack(old_c, new_c, lens, idx, val); });
+}
+
+int sskm_local_candidates(sskm_ctx* ctx, int64_t m, double* sims, int64_t* gids, uint32_t* clusters,
+                          int64_t* m_out) {
+    return guard([&] { *m_out = E(ctx).local_candidates(m, sims, gids, clusters); });
+}
+
+int sskm_init_from_rows(sskm_ctx* ctx, const int64_t* row_ptr, const int32_t* idx, const float* val) {
+    return guard([&] { E(ctx).init_from_rows(row_ptr, idx, val); });
 }
 
 int sskm_update_apply(sskm_ctx* ctx, int64_t n_moved, const uint32_t* old_c, const uint32_t* new_c,

@@ -140,6 +140,54 @@ __global__ void delta_packed_kernel(int64_t n_moved, const uint32_t* __restrict_
     }
 }
 
+// Multi-GPU delta exchange: per moved document its (old, new) clusters and
+// row length, then (after a scan) the rows themselves, packed contiguously.
+__global__ void moved_meta_kernel(const uint32_t* __restrict__ moved, const unsigned long long* n_moved_p,
+                                  const int64_t* __restrict__ indptr, const uint32_t* __restrict__ a,
+                                  const uint32_t* __restrict__ a_sum, int64_t* __restrict__ lens,
+                                  uint32_t* __restrict__ old_c, uint32_t* __restrict__ new_c) {
+    const uint64_t n_moved = *n_moved_p;
+    for (uint64_t m = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; m <= n_moved;
+         m += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (m == n_moved) {
+            lens[m] = 0;
+            continue;
+        }
+        const uint32_t i = moved[m];
+        lens[m] = indptr[i + 1] - indptr[i];
+        old_c[m] = a_sum[i];
+        new_c[m] = a[i];
+    }
+}
+
+__global__ void pack_rows_kernel(const uint32_t* __restrict__ moved, int64_t n_moved,
+                                 const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                 const float* __restrict__ val, const int64_t* __restrict__ offs,
+                                 int32_t* __restrict__ lens32, int32_t* __restrict__ idx_out,
+                                 float* __restrict__ val_out) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t m = gw; m < static_cast<uint64_t>(n_moved); m += nw) {
+        const uint32_t i = moved[m];
+        const int64_t b = indptr[i], e = indptr[i + 1], o = offs[m];
+        for (int64_t q = b + lane; q < e; q += kWarp) {
+            idx_out[o + (q - b)] = idx[q];
+            val_out[o + (q - b)] = val[q];
+        }
+        if (lane == 0) lens32[m] = static_cast<int32_t>(e - b);
+    }
+}
+
+__global__ void scatter_rows_kernel(const int64_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
+                                    const float* __restrict__ rval, uint32_t k, float* __restrict__ CT, uint64_t ld) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const uint32_t nw = gridDim.x * blockDim.x / kWarp;
+    for (uint32_t j = gw; j < k; j += nw)
+        for (int64_t e = rptr[j] + lane; e < rptr[j + 1]; e += kWarp) CT[static_cast<uint64_t>(ridx[e]) * ld + j] = rval[e];
+}
+
 // Ascending compaction of {j : flag(j)} in one block (k ≤ a few 1e5).
 // want = 1: keep flag != 0; want = 0: keep flag == 0.
 __global__ void compact_ids_kernel(const uint8_t* __restrict__ flags, uint32_t k, int want,
