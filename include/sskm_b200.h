@@ -80,6 +80,7 @@ typedef struct {
     double screen_ms;         /* device time of the postings-screen kernel launches only */
     uint32_t screen_launches; /* postings-screen launches in this assign (one per cluster tile) */
     uint32_t reserved0;
+    double centroid_density;  /* nonzero fraction of the centroid tile last indexed (screen choice) */
 } sskm_iteration_stats;
 
 typedef struct sskm_ctx sskm_ctx;

@@ -59,6 +59,7 @@ class sskm_iteration_stats(C.Structure):
         ("screen_ms", C.c_double),
         ("screen_launches", C.c_uint32),
         ("reserved0", C.c_uint32),
+        ("centroid_density", C.c_double),
     ]
 
 

@@ -118,6 +118,7 @@ class IterationStats:
     screen_ms: float = 0.0
     screen_launches: int = 0
     reserved0: int = 0
+    centroid_density: float = 0.0
 
     @classmethod
     def from_c(cls, s: sskm_iteration_stats) -> "IterationStats":

@@ -581,6 +581,7 @@ struct ResolveArgs {
     const uint32_t* order;
     int64_t n_work;
     double cmax;               // upper bound on every centroid column's 2-norm
+    int nonneg;                // all document weights > 0 (so centroids >= 0): relative bound
     const float* sb;
     const float* ss;
     const uint32_t* sa;
@@ -619,6 +620,15 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
         const double delta = (g32 + g64) * sqrt(q) * (1.0 + 1e-12) * p.cmax * (1.0 + 1e-12);
         const float b = p.sb[i], s2 = p.ss[i];
         const uint32_t sa = p.sa[i];
+        // Error model of a screened value s32 against the reference's fp64 s64:
+        //  signed data:      |s32 − s64| ≤ δ                        (absolute, Cauchy–Schwarz)
+        //  nonnegative data: |s32 − s64| ≤ g'·s32, g' = g/(1−g) + γ64 (Σ|x_t c_t| = s itself)
+        const double g = g32 / (1.0 - g32) + g64 + 1e-15;
+        // (+ n·2^-126 absolute: fp32 products below the normal range)
+        const double tiny = n * 0x1p-126;
+        auto upper = [&](double v) { return p.nonneg ? (v >= 0.0 ? v * (1.0 + g) : v * (1.0 - g)) + tiny : v + delta; };
+        auto lower = [&](double v) { return p.nonneg ? (v >= 0.0 ? v * (1.0 - g) : v * (1.0 + g)) - tiny : v - delta; };
+        const double bd = static_cast<double>(b), s2d = static_cast<double>(s2);
         double best;
         uint32_t arg;
         bool certain;
@@ -627,7 +637,7 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
         if constexpr (INIT == kInitFull) {
             // the screen covered every column; the reference's (-2, 0) start only
             // survives when every similarity is <= -2 (left to the exact scan)
-            certain = sa != kNone && static_cast<double>(b) - static_cast<double>(s2) > 2.0 * delta;
+            certain = sa != kNone && lower(bd) > upper(s2d);
             best = 0.0;
             arg = sa;
             if (certain) {
@@ -644,10 +654,9 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
                                             : old_sim;
             best = sim0;
             arg = a0;
-            if (sa == kNone || static_cast<double>(b) < sim0 - delta) {
+            if (sa == kNone || upper(bd) < sim0) {
                 certain = true;  // no screened column can reach the baseline
-            } else if (static_cast<double>(b) - delta > sim0 &&
-                       static_cast<double>(b) - static_cast<double>(s2) > 2.0 * delta) {
+            } else if (lower(bd) > sim0 && lower(bd) > upper(s2d)) {
                 best = doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, sa, lane);
                 arg = sa;
                 certain = true;

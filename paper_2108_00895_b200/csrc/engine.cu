@@ -84,6 +84,7 @@ public:
         if (const char* e = std::getenv("SSKM_SCREEN_UNROLL")) screen_unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_POST_UNROLL")) post_unroll_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_DENSE_ABOVE")) dense_above_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_SCREEN_KIND")) screen_kind_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_SCREEN")) screen_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SCREEN_BLOCKS_PER_SM")) screen_blocks_per_sm_ = std::max(1, std::atoi(e));
@@ -167,6 +168,7 @@ public:
         if (hs_->bad & 4u) throw InvalidArgument("SparseVector: zero weight");
         if (hs_->bad & 8u)
             throw InvalidArgument("document weights must be finite with |x| <= 1 (unit-length rows)");
+        nonneg_ = (hs_->bad & 16u) == 0;
         // fixed-point scale: N_total · 2^K <= 2^62 with |x| <= 1
         int lg = 0;
         while ((int64_t(1) << lg) < n_total_) ++lg;
@@ -1022,7 +1024,24 @@ private:
 
     void screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
                     const uint32_t* order, int64_t n_work) {
-        if (screen_kind_ == 1)
+        // postings move 8 B per nonzero centroid weight at ~4 TB/s, the dense
+        // screen 4 B per weight mostly from L2 at ~12 TB/s: above ~15% density
+        // (long documents, few clusters: c3) the dense screen wins (measured)
+        if (screen_kind_ == 2 && last_density_ > dense_above_ && (++dense_assigns_ % 5) == 0) {
+            // re-measure the density every few dense assigns (one count pass over tile 0)
+            const uint32_t kt = std::min<uint32_t>(ncols, 2048);
+            CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
+            launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, 0u, kt,
+                   pcnt_.p);
+            size_t tmp = scan_tmp_.n;
+            CK(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
+            uint32_t total = 0;
+            CK(cudaMemcpyAsync(&total, pptr_.p + d_, 4, cudaMemcpyDeviceToHost, stream_));
+            CK(cudaStreamSynchronize(stream_));
+            last_density_ = static_cast<double>(total) / (static_cast<double>(d_) * kt);
+        }
+        const bool use_postings = screen_kind_ == 1 || (screen_kind_ == 2 && last_density_ <= dense_above_);
+        if (use_postings)
             postings_screen(M, ld, ncols, col_ids, skip, order, n_work);
         else
             screen_tiles(M, ld, ncols, col_ids, skip, order, n_work);
@@ -1070,6 +1089,7 @@ private:
                    pptr_.p, pairs_.p);
             p.pptr = pptr_.p;
             p.pairs = pairs_.p;
+            if (c0 == 0) last_density_ = static_cast<double>(total) / (static_cast<double>(d_) * kt);
             p.c0 = c0;
             p.kt = kt;
             p.first = c0 == 0;
@@ -1205,6 +1225,7 @@ private:
         r.order = order;
         r.n_work = n_work;
         r.cmax = cmax_;
+        r.nonneg = nonneg_ ? 1 : 0;
         r.sb = sb_.p;
         r.ss = ss_.p;
         r.sa = sa_.p;
@@ -1266,6 +1287,7 @@ private:
         st->assign_kernel_ms = kms;
         st->screen_ms = screen_ms_;
         st->screen_launches = screen_launches_;
+        st->centroid_density = last_density_;
     }
 
     int device_;
@@ -1310,9 +1332,13 @@ private:
     int64_t postings_total_ = 0;
     double screen_ms_ = 0.0;
     uint32_t screen_launches_ = 0;
-    int screen_kind_ = 1;
+    int screen_kind_ = 2;  // 0 dense, 1 postings, 2 by measured density
     int post_unroll_ = 8;
     bool cache_trusted_ = false;
+    bool nonneg_ = true;
+    double last_density_ = 0.0;
+    double dense_above_ = 0.15;
+    uint64_t dense_assigns_ = 0;
     double ncc_full_frac_ = 0.25;
     DevBuf<uint32_t> sa_, exact_;
     DevBuf<uint32_t> order_, keys32_;
@@ -1386,6 +1412,7 @@ void step(Engine& e, sskm_iteration_stats* st) {
     st->assign_kernel_ms = a.assign_kernel_ms;
     st->screen_ms = a.screen_ms;
     st->screen_launches = a.screen_launches;
+    st->centroid_density = a.centroid_density;
     st->n_exact = a.n_exact;
     st->index_active = 0;
     st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

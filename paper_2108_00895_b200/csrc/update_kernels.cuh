@@ -388,6 +388,7 @@ __global__ void validate_csr_kernel(const int64_t* __restrict__ indptr, const in
             if (t <= prev || t < 0 || static_cast<uint32_t>(t) >= dims) atomicOr(bad, 2u);
             if (x == 0.f) atomicOr(bad, 4u);
             if (!(fabsf(x) <= 1.0f)) atomicOr(bad, 8u);
+            if (x < 0.f) atomicOr(bad, 16u);  // not an error: signed corpus (absolute screen bound)
             prev = t;
         }
     }
