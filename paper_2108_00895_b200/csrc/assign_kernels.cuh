@@ -454,12 +454,20 @@ __device__ __forceinline__ uint2 ld_pair(const uint2* p, uint64_t pol) {
     return pr;
 }
 
-template <int KT, int U>
+// SUB lanes serve one posting list; the warp's G = 32/SUB lane groups work on
+// G consecutive terms at once, each group into its own KT-float accumulator
+// (no conflicts between groups; clusters within a list are distinct). The G
+// partial sums are added in a fixed order at the end. Any summation order
+// obeys the same γ(n + 32) bound, which the resolve step uses.
+template <int KT, int SUB>
 __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
+    constexpr int G = kWarp / SUB;
     extern __shared__ float smem_acc[];
     const int lane = threadIdx.x & (kWarp - 1);
+    const int grp = lane / SUB, sl = lane % SUB;
     const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
-    float* acc = smem_acc + static_cast<size_t>(warp) * KT;
+    float* accw = smem_acc + static_cast<size_t>(warp) * G * KT;
+    float* accg = accw + grp * KT;
     const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_work, gridDim.x));
     const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
     const int64_t w1 = imin64(p.n_work, w0 + chunk);
@@ -469,8 +477,8 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
         const int64_t beg = __ldg(p.indptr + i), end = __ldg(p.indptr + i + 1);
         const uint32_t skip = p.skip_id ? __ldg(p.skip_id + i) : kNone;
 #pragma unroll
-        for (int c = lane * 4; c < KT; c += kWarp * 4)
-            *reinterpret_cast<float4*>(acc + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = lane * 4; c < G * KT; c += kWarp * 4)
+            *reinterpret_cast<float4*>(accw + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
         for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
             const int64_t e = e0 + lane;
@@ -483,24 +491,53 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
                 le = __ldg(p.pptr + t + 1);
             }
             const int n = static_cast<int>(imin64(kWarp, end - e0));
-            for (int j = 0; j < n; ++j) {
-                const uint32_t qb = __shfl_sync(0xFFFFFFFFu, lb, j);
-                const uint32_t qe = __shfl_sync(0xFFFFFFFFu, le, j);
-                const float x = __shfl_sync(0xFFFFFFFFu, x_l, j);
-                for (uint32_t q = qb + lane; q < qe; q += kWarp) {
-                    const uint2 pr = ld_pair(p.pairs + q, pol_keep);
-                    acc[pr.x] = fmaf(x, __uint_as_float(pr.y), acc[pr.x]);
+            if constexpr (G == 1) {
+                // one warp per list, next term's first 32 postings prefetched
+                // while the current term accumulates (hides one L2 round trip)
+                uint32_t qb = __shfl_sync(0xFFFFFFFFu, lb, 0) + lane, qe = __shfl_sync(0xFFFFFFFFu, le, 0);
+                float x = __shfl_sync(0xFFFFFFFFu, x_l, 0);
+                uint2 pr = qb < qe ? ld_pair(p.pairs + qb, pol_keep) : make_uint2(0u, 0u);
+                for (int j = 0; j < n; ++j) {
+                    const int jn = (j + 1) & (kWarp - 1);
+                    uint32_t nb = __shfl_sync(0xFFFFFFFFu, lb, jn) + lane, ne = __shfl_sync(0xFFFFFFFFu, le, jn);
+                    const float nx = __shfl_sync(0xFFFFFFFFu, x_l, jn);
+                    if (j + 1 >= n) ne = 0;
+                    const uint2 npr = nb < ne ? ld_pair(p.pairs + nb, pol_keep) : make_uint2(0u, 0u);
+                    if (qb < qe) accg[pr.x] = fmaf(x, __uint_as_float(pr.y), accg[pr.x]);
+                    for (uint32_t q = qb + kWarp; q < qe; q += kWarp) {
+                        const uint2 t2 = ld_pair(p.pairs + q, pol_keep);
+                        accg[t2.x] = fmaf(x, __uint_as_float(t2.y), accg[t2.x]);
+                    }
+                    __syncwarp();
+                    qb = nb;
+                    qe = ne;
+                    x = nx;
+                    pr = npr;
                 }
-                __syncwarp();
+            } else {
+                for (int j0 = 0; j0 < n; j0 += G) {
+                    const int j = j0 + grp;  // lanes past n hold empty lists
+                    const uint32_t qb = __shfl_sync(0xFFFFFFFFu, lb, j);
+                    const uint32_t qe = __shfl_sync(0xFFFFFFFFu, le, j);
+                    const float x = __shfl_sync(0xFFFFFFFFu, x_l, j);
+                    for (uint32_t q = qb + sl; q < qe; q += SUB) {
+                        const uint2 pr = ld_pair(p.pairs + q, pol_keep);
+                        accg[pr.x] = fmaf(x, __uint_as_float(pr.y), accg[pr.x]);
+                    }
+                    __syncwarp();
+                }
             }
         }
-        // top-2 over the tile's clusters
+        // combine the G partial accumulators (fixed order), then top-2
         float tb = -INFINITY, ts2 = -INFINITY;
         uint32_t ta = kNone;
         for (int c = lane; c < static_cast<int>(p.kt); c += kWarp) {
+            float v = accw[c];
+#pragma unroll
+            for (int g = 1; g < G; ++g) v += accw[g * KT + c];
             const uint32_t col = p.c0 + static_cast<uint32_t>(c);
             const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
-            if (id != skip) top2_push(acc[c], id, tb, ta, ts2);
+            if (id != skip) top2_push(v, id, tb, ta, ts2);
         }
         warp_top2(tb, ta, ts2);
         if (lane == 0) {
@@ -616,7 +653,8 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
         for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, off);
         const double n = static_cast<double>(end - beg);
         const double u32 = 0x1p-24, u64 = 0x1p-53;
-        const double g32 = n * u32 / (1.0 - n * u32), g64 = n * u64 / (1.0 - n * u64);
+        const double n32 = n + 32.0;  // screen: any summation order, up to 32 partial sums
+        const double g32 = n32 * u32 / (1.0 - n32 * u32), g64 = n * u64 / (1.0 - n * u64);
         const double delta = (g32 + g64) * sqrt(q) * (1.0 + 1e-12) * p.cmax * (1.0 + 1e-12);
         const float b = p.sb[i], s2 = p.ss[i];
         const uint32_t sa = p.sa[i];

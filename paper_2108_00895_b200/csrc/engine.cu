@@ -83,7 +83,8 @@ public:
         if (const char* e = std::getenv("SSKM_UNROLL")) unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_SCREEN_UNROLL")) screen_unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
-        if (const char* e = std::getenv("SSKM_POST_UNROLL")) post_unroll_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_POST_SUB")) post_sub_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_POST_WARPS")) post_warps_ = std::max(1, std::min(8, std::atoi(e)));
         if (const char* e = std::getenv("SSKM_DENSE_ABOVE")) dense_above_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_SCREEN_KIND")) screen_kind_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_SCREEN")) screen_enabled_ = std::atoi(e) != 0;
@@ -1136,23 +1137,27 @@ public:
 private:
     template <int KT>
     void postings_launch(const PostingsArgs& p, int64_t n_work) {
-        if (post_unroll_ >= 8)
-            postings_launch_u<KT, 8>(p, n_work);
+        if (post_sub_ >= 32)
+            postings_launch_s<KT, 32>(p, n_work);
+        else if (post_sub_ >= 16)
+            postings_launch_s<KT, 16>(p, n_work);
         else
-            postings_launch_u<KT, 4>(p, n_work);
+            postings_launch_s<KT, 8>(p, n_work);
     }
 
-    template <int KT, int U>
-    void postings_launch_u(const PostingsArgs& p, int64_t n_work) {
-        auto k = postings_screen_kernel<KT, U>;
-        const size_t smem = static_cast<size_t>(8) * KT * sizeof(float);
+    template <int KT, int SUB>
+    void postings_launch_s(const PostingsArgs& p, int64_t n_work) {
+        auto k = postings_screen_kernel<KT, SUB>;
+        const size_t per_warp = static_cast<size_t>(32 / SUB) * KT * sizeof(float);
+        const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(post_warps_, (200u << 10) / per_warp)));
+        const size_t smem = static_cast<size_t>(warps) * per_warp;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem));
         per_sm = std::max(1, per_sm);
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(n_work, 8))));
-        k<<<grid, 256, smem, stream_>>>(p);
+            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(n_work, warps))));
+        k<<<grid, warps * 32, smem, stream_>>>(p);
         ++launches_;
     }
 
@@ -1333,7 +1338,8 @@ private:
     double screen_ms_ = 0.0;
     uint32_t screen_launches_ = 0;
     int screen_kind_ = 2;  // 0 dense, 1 postings, 2 by measured density
-    int post_unroll_ = 8;
+    int post_sub_ = 16;
+    int post_warps_ = 8;
     bool cache_trusted_ = false;
     bool nonneg_ = true;
     double last_density_ = 0.0;

@@ -9,7 +9,8 @@ cfg = S.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c1"]
 data = S.corpus(cfg)
 seeds = S.init_seeds(data.n_docs, cfg.k, 0)
 variants = [dict(SSKM_SCREEN="0", SSKM_TILE_BYTES=str(128 << 20), SSKM_ORDER="1", SSKM_UNROLL="16")]
-variants += [dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="1", SSKM_ORDER=str(o), SSKM_POST_UNROLL=str(u)) for o in (0, 1) for u in (4, 8)]
+variants += [dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="1", SSKM_ORDER=str(o), SSKM_POST_SUB="32", SSKM_POST_WARPS=str(w))
+             for o in (0, 1) for w in (4, 8)]
 ref_a = None
 for v in variants:
     os.environ.update(v)
@@ -30,5 +31,5 @@ for v in variants:
     else:
         same = bool(np.array_equal(a, ref_a) and np.array_equal(s, ref_s))
     print(json.dumps(dict(v, n_exact=int(np.mean([x.n_exact for x in sts])), ms_iter=round(ms, 3), assign_kernel_ms=round(float(np.mean([x.assign_kernel_ms for x in sts])), 3),
-                          update_ms=round(float(np.mean([x.update_ms for x in sts])), 3), same_as_first=same)), flush=True)
+                          update_ms=round(float(np.mean([x.update_ms for x in sts])), 3), screen_ms=round(float(np.mean([x.screen_ms for x in sts])), 3), same_as_first=same)), flush=True)
     eng.close()

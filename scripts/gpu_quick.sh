@@ -1,2 +1,2 @@
 set -x
-timeout 1200 python -m pytest tests/test_gpu_distributed.py -x -q > gpurun_out/pytest_gpu_dist.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_gpu_dist.log
+timeout 2400 python -m pytest tests/test_gpu_parity.py -x -q -k large_sampled --durations=5 > gpurun_out/pytest_large.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_large.log
