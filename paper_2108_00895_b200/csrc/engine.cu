@@ -84,6 +84,7 @@ public:
         if (const char* e = std::getenv("SSKM_SCREEN_UNROLL")) screen_unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_POST_SUB")) post_sub_ = std::atoi(e);
+        if (const char* e = std::getenv("SSKM_POST_KT")) post_kt_max_ = static_cast<uint32_t>(std::atoi(e));
         if (const char* e = std::getenv("SSKM_POST_WARPS")) post_warps_ = std::max(1, std::min(8, std::atoi(e)));
         if (const char* e = std::getenv("SSKM_DENSE_ABOVE")) dense_above_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_SCREEN_KIND")) screen_kind_ = std::atoi(e);
@@ -1058,7 +1059,7 @@ private:
         pcnt_.alloc(d_ + 1);
         pptr_.alloc(d_ + 1);
         // tile pairs are addressed with 32-bit offsets: d · KT < 2^32
-        const uint32_t KT = ncols <= 256 ? 256 : (ncols <= 1024 ? 1024 : 2048);
+        const uint32_t KT = post_tile_width(ncols);
         if (static_cast<uint64_t>(d_) * KT >= (1ull << 32)) throw InvalidArgument("vocabulary too large for postings");
         PostingsArgs p{};
         p.indptr = indptr_.p;
@@ -1098,6 +1099,8 @@ private:
             CK(cudaEventRecord(ev_[6], stream_));
             if (KT == 256)
                 postings_launch<256>(p, n_work);
+            else if (KT == 512)
+                postings_launch<512>(p, n_work);
             else if (KT == 1024)
                 postings_launch<1024>(p, n_work);
             else
@@ -1119,7 +1122,7 @@ public:
         need_state();
         reset_scalars();
         uint64_t total = 0;
-        const uint32_t KT = k_ <= 256 ? 256 : (k_ <= 1024 ? 1024 : 2048);
+        const uint32_t KT = post_tile_width(k_);
         for (uint32_t c0 = 0; c0 < k_; c0 += KT) {
             const uint32_t kt = std::min<uint32_t>(KT, k_ - c0);
             CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
@@ -1135,6 +1138,16 @@ public:
     }
 
 private:
+    // Cluster-tile width of the postings screen: the per-warp accumulator is
+    // KT floats of shared memory, so narrower tiles buy occupancy (the screen
+    // is latency-bound) at the price of one more CSR pass per tile.
+    uint32_t post_tile_width(uint32_t ncols) const {
+        if (ncols <= 256) return 256;
+        if (ncols <= 512 || post_kt_max_ <= 512) return 512;
+        if (ncols <= 1024 || post_kt_max_ <= 1024) return 1024;
+        return 2048;
+    }
+
     template <int KT>
     void postings_launch(const PostingsArgs& p, int64_t n_work) {
         if (post_sub_ >= 32)
@@ -1338,7 +1351,8 @@ private:
     double screen_ms_ = 0.0;
     uint32_t screen_launches_ = 0;
     int screen_kind_ = 2;  // 0 dense, 1 postings, 2 by measured density
-    int post_sub_ = 16;
+    int post_sub_ = 32;
+    uint32_t post_kt_max_ = 1024;
     int post_warps_ = 8;
     bool cache_trusted_ = false;
     bool nonneg_ = true;

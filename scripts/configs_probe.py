@@ -17,3 +17,7 @@ for it in range(1, iters + 1):
                           assign_ms=round(st.assign_ms, 2), screen_ms=round(st.screen_ms, 2), tiles=st.screen_launches,
                           n_changed=st.n_changed, density=round(st.centroid_density, 4), n_reassigned=st.n_reassigned, n_exact=st.n_exact,
                           n_rescan=st.n_rescan, n_repaired=st.n_repaired, dots=st.dot_products)), flush=True)
+if os.environ.get("PROBE_PAIRS"):
+    pairs = eng.postings_work()
+    print(json.dumps(dict(postings_pairs=pairs, mean_dfc_per_entry=pairs / data.nnz,
+                          density_weighted_ratio=pairs / (data.nnz * cfg.k))), flush=True)
