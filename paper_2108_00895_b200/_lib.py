@@ -136,9 +136,8 @@ def load():
     if _build.stale():
         try:
             _build.build()
-        except Exception as e:  # no silent fallback
-            if not os.path.exists(_build.LIB):
-                raise ImportError(f"libsskm_b200.so is missing and could not be built: {e}") from e
+        except Exception as e:  # no silent fallback, and never a stale binary
+            raise ImportError(f"libsskm_b200.so is missing or out of date and could not be built: {e}") from e
     lib = C.CDLL(_build.LIB)
     for name, res, args in SIGNATURES:
         fn = getattr(lib, name)

@@ -572,7 +572,12 @@ __global__ void postings_work_kernel(const int32_t* __restrict__ idx, int64_t nn
 }
 
 // Postings build from the dense column tile [c0, c0 + kt) of M: per-row counts,
-// then (after an exclusive scan) the pairs in ascending cluster order.
+// then (after an exclusive scan) the pairs. Within a list the pairs are laid
+// out round-robin by shared-memory bank (rank-0 pair of every bank, then
+// rank-1, ...), so the 32 pairs a warp processes together mostly hit distinct
+// accumulator banks. Lane l scans columns j = l (mod 32), i.e. exactly bank l
+// (tiles start at multiples of 32). The order inside one list never changes a
+// result: every cluster occurs once per list.
 __global__ void postings_count_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d, uint32_t c0,
                                       uint32_t kt, uint32_t* __restrict__ cnt) {
     const int lane = threadIdx.x & (kWarp - 1);
@@ -588,24 +593,41 @@ __global__ void postings_count_kernel(const float* __restrict__ M, uint64_t ld, 
     }
 }
 
-__global__ void postings_fill_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d, uint32_t c0,
-                                     uint32_t kt, const uint32_t* __restrict__ pptr, uint2* __restrict__ pairs) {
+__global__ void __launch_bounds__(256) postings_fill_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
+                                                            uint32_t c0, uint32_t kt, const uint32_t* __restrict__ pptr,
+                                                            uint2* __restrict__ pairs) {
+    constexpr int kMaxRank = 64;  // kt <= 2048 clusters per tile
+    __shared__ uint32_t s_mask[8][kMaxRank], s_base[8][kMaxRank];
     const int lane = threadIdx.x & (kWarp - 1);
+    const int wib = (threadIdx.x / kWarp) & 7;
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    const unsigned lt = (1u << lane) - 1u;
+    const int ranks = static_cast<int>((kt + kWarp - 1) / kWarp);
     for (uint64_t t = gw; t < d; t += nw) {
         const float* row = M + t * ld + c0;
-        uint32_t pos = pptr[t];
-        for (uint32_t j0 = 0; j0 < kt; j0 += kWarp) {
-            const uint32_t j = j0 + lane;
-            const float v = j < kt ? row[j] : 0.f;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, v != 0.f);
-            if (v != 0.f) {
-                const int r = __popc(bal & ((1u << lane) - 1u));
-                pairs[pos + r] = make_uint2(j, __float_as_uint(v));
+        uint32_t cnt = 0;
+        for (uint32_t j = lane; j < kt; j += kWarp) cnt += row[j] != 0.f;
+        uint32_t run = 0;
+        for (int r = 0; r < ranks; ++r) {
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, cnt > static_cast<uint32_t>(r));
+            if (lane == 0) {
+                s_mask[wib][r] = m;
+                s_base[wib][r] = run;
             }
-            pos += __popc(bal);
+            run += __popc(m);
         }
+        __syncwarp();
+        const uint32_t base = pptr[t];
+        uint32_t r = 0;
+        for (uint32_t j = lane; j < kt; j += kWarp) {
+            const float v = row[j];
+            if (v != 0.f) {
+                pairs[base + s_base[wib][r] + __popc(s_mask[wib][r] & lt)] = make_uint2(j, __float_as_uint(v));
+                ++r;
+            }
+        }
+        __syncwarp();
     }
 }
 
