@@ -353,6 +353,31 @@ __device__ __forceinline__ void warp_top2(float& b, uint32_t& a, float& s2) {
     }
 }
 
+struct ResolveArgs {
+    const int64_t* indptr;
+    const int32_t* idx;
+    const float* val;
+    const float* CT;
+    uint64_t ld_ct;
+    const uint32_t* order;
+    int64_t n_work;
+    double cmax;               // upper bound on every centroid column's 2-norm
+    int nonneg;                // all document weights > 0 (so centroids >= 0): relative bound
+    const float* sb;
+    const float* ss;
+    const uint32_t* sa;
+    // NCC
+    const uint8_t* unchanged;
+    const uint32_t* a_start;
+    const double* sims_start;
+    uint32_t* a;
+    double* sims;
+    uint32_t* exact_list;      // uncertified documents -> exact fp64 scan
+    unsigned long long* n_exact;
+    uint32_t* rescan_list;
+    unsigned long long* n_rescan;
+};
+
 struct ScreenArgs {
     const int64_t* indptr;
     const int32_t* idx;
@@ -446,7 +471,12 @@ struct PostingsArgs {
     float* sb;
     float* ss;
     uint32_t* sa;
+    ResolveArgs r;             // used when the last tile certifies in place (FUSE >= 0)
 };
+
+template <int INIT>
+__device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int64_t beg, int64_t end, int lane,
+                                            float b, float s2, uint32_t sa);
 
 __device__ __forceinline__ uint2 ld_pair(const uint2* p, uint64_t pol) {
     uint2 pr;
@@ -459,7 +489,7 @@ __device__ __forceinline__ uint2 ld_pair(const uint2* p, uint64_t pol) {
 // (no conflicts between groups; clusters within a list are distinct). The G
 // partial sums are added in a fixed order at the end. Any summation order
 // obeys the same γ(n + 32) bound, which the resolve step uses.
-template <int KT, int SUB>
+template <int KT, int SUB, int FUSE>
 __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
     constexpr int G = kWarp / SUB;
     extern __shared__ float smem_acc[];
@@ -504,6 +534,8 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
                     if (j + 1 >= n) ne = 0;
                     const uint2 npr = nb < ne ? ld_pair(p.pairs + nb, pol_keep) : make_uint2(0u, 0u);
                     if (qb < qe) accg[pr.x] = fmaf(x, __uint_as_float(pr.y), accg[pr.x]);
+                    // most lists fit the prefetched first 32; keep the rare tail compact
+#pragma unroll 1
                     for (uint32_t q = qb + kWarp; q < qe; q += kWarp) {
                         const uint2 t2 = ld_pair(p.pairs + q, pol_keep);
                         accg[t2.x] = fmaf(x, __uint_as_float(t2.y), accg[t2.x]);
@@ -540,18 +572,21 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
             if (id != skip) top2_push(v, id, tb, ta, ts2);
         }
         warp_top2(tb, ta, ts2);
-        if (lane == 0) {
-            float b = -INFINITY, s2 = -INFINITY;
-            uint32_t a = kNone;
-            if (!p.first) {
-                b = p.sb[i];
-                s2 = p.ss[i];
-                a = p.sa[i];
-            }
-            if (ta != kNone) {
-                top2_push(tb, ta, b, a, s2);
-                s2 = fmaxf(s2, ts2);
-            }
+        float b = -INFINITY, s2 = -INFINITY;
+        uint32_t a = kNone;
+        if (!p.first) {
+            b = p.sb[i];
+            s2 = p.ss[i];
+            a = p.sa[i];
+        }
+        if (ta != kNone) {
+            top2_push(tb, ta, b, a, s2);
+            s2 = fmaxf(s2, ts2);
+        }
+        if constexpr (FUSE >= 0) {
+            // last cluster tile: certify here instead of in a separate pass
+            resolve_doc<FUSE>(p.r, i, beg, end, lane, b, s2, a);
+        } else if (lane == 0) {
             p.sb[i] = b;
             p.ss[i] = s2;
             p.sa[i] = a;
@@ -631,40 +666,12 @@ __global__ void __launch_bounds__(256) postings_fill_kernel(const float* __restr
     }
 }
 
-struct ResolveArgs {
-    const int64_t* indptr;
-    const int32_t* idx;
-    const float* val;
-    const float* CT;
-    uint64_t ld_ct;
-    const uint32_t* order;
-    int64_t n_work;
-    double cmax;               // upper bound on every centroid column's 2-norm
-    int nonneg;                // all document weights > 0 (so centroids >= 0): relative bound
-    const float* sb;
-    const float* ss;
-    const uint32_t* sa;
-    // NCC
-    const uint8_t* unchanged;
-    const uint32_t* a_start;
-    const double* sims_start;
-    uint32_t* a;
-    double* sims;
-    uint32_t* exact_list;      // uncertified documents -> exact fp64 scan
-    unsigned long long* n_exact;
-    uint32_t* rescan_list;
-    unsigned long long* n_rescan;
-};
-
-// Certify the screen's answer per document (warp per document).
+// Certify one document's screen result (b, s2, sa) and write the exact answer
+// (or queue the document for the exact scan). Called by resolve_kernel and,
+// fused, by the screen kernels on their last cluster tile.
 template <int INIT>
-__global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
-    const int lane = threadIdx.x & (kWarp - 1);
-    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
-    for (uint64_t w = gw; w < static_cast<uint64_t>(p.n_work); w += nw) {
-        const int64_t i = p.order ? static_cast<int64_t>(p.order[w]) : static_cast<int64_t>(w);
-        const int64_t beg = p.indptr[i], end = p.indptr[i + 1];
+__device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int64_t beg, int64_t end, int lane,
+                                            float b, float s2, uint32_t sa) {
         // ||x||₂ (fp64) for the error bound
         double q = 0.0;
         for (int64_t e = beg + lane; e < end; e += kWarp) {
@@ -678,8 +685,6 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
         const double n32 = n + 32.0;  // screen: any summation order, up to 32 partial sums
         const double g32 = n32 * u32 / (1.0 - n32 * u32), g64 = n * u64 / (1.0 - n * u64);
         const double delta = (g32 + g64) * sqrt(q) * (1.0 + 1e-12) * p.cmax * (1.0 + 1e-12);
-        const float b = p.sb[i], s2 = p.ss[i];
-        const uint32_t sa = p.sa[i];
         // Error model of a screened value s32 against the reference's fp64 s64:
         //  signed data:      |s32 − s64| ≤ δ                        (absolute, Cauchy–Schwarz)
         //  nonnegative data: |s32 − s64| ≤ g'·s32, g' = g/(1−g) + γ64 (Σ|x_t c_t| = s itself)
@@ -739,6 +744,17 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
                 p.exact_list[pos] = static_cast<uint32_t>(i);
             }
         }
+}
+
+// Certify the screen's answer per document (warp per document).
+template <int INIT>
+__global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t w = gw; w < static_cast<uint64_t>(p.n_work); w += nw) {
+        const int64_t i = p.order ? static_cast<int64_t>(p.order[w]) : static_cast<int64_t>(w);
+        resolve_doc<INIT>(p, i, p.indptr[i], p.indptr[i + 1], lane, p.sb[i], p.ss[i], p.sa[i]);
     }
 }
 

@@ -83,6 +83,7 @@ public:
         if (const char* e = std::getenv("SSKM_UNROLL")) unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_SCREEN_UNROLL")) screen_unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
+        if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_POST_SUB")) post_sub_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_POST_KT")) post_kt_max_ = static_cast<uint32_t>(std::atoi(e));
         if (const char* e = std::getenv("SSKM_POST_WARPS")) post_warps_ = std::max(1, std::min(8, std::atoi(e)));
@@ -424,8 +425,7 @@ public:
         CK(cudaEventRecord(ev_[4], stream_));
         uint64_t n_exact = 0;
         if (screen_enabled_) {
-            screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_);
-            resolve<kInitFull>(order, n_);
+            if (!screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_, kInitFull)) resolve<kInitFull>(order, n_);
             pull_scalars();
             n_exact = hs_->n_exact;
             if (n_exact > 0) scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(n_exact));
@@ -458,8 +458,7 @@ public:
         const bool full_equiv = cfg_.ncc_epsilon == 0.0 && cache_trusted_ && screen_enabled_ &&
                                 static_cast<double>(n_chg_) >= ncc_full_frac_ * k_;
         if (n_chg_ > 0 && full_equiv) {
-            screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_);
-            resolve<kInitFull>(order, n_);
+            if (!screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_, kInitFull)) resolve<kInitFull>(order, n_);
             pull_scalars();
             n_exact = hs_->n_exact;
             if (n_exact > 0) scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(n_exact));
@@ -471,8 +470,8 @@ public:
             n_rescan = hs_->n_rescan;
         } else if (n_chg_ > 0) {
             if (screen_enabled_) {
-                screen_any(cc_.p, ld_cc_, n_chg_, chg_ids_.p, a_start_.p, order, n_);
-                resolve<kInitNcc>(order, n_);
+                if (!screen_any(cc_.p, ld_cc_, n_chg_, chg_ids_.p, a_start_.p, order, n_, kInitNcc))
+                    resolve<kInitNcc>(order, n_);
                 pull_scalars();
                 n_exact = hs_->n_exact;
                 if (n_exact > 0)
@@ -486,8 +485,8 @@ public:
                 // pass B over all centroids for the rescan documents (engine.cpp:303-305)
                 if (screen_enabled_) {
                     CK(cudaMemsetAsync(&scal_.p->n_exact, 0, 8, stream_));
-                    screen_any(ct_.p, ld_, k_, nullptr, a_.p, rescan_.p, static_cast<int64_t>(n_rescan));
-                    resolve<kInitRescan>(rescan_.p, static_cast<int64_t>(n_rescan));
+                    if (!screen_any(ct_.p, ld_, k_, nullptr, a_.p, rescan_.p, static_cast<int64_t>(n_rescan), kInitRescan))
+                        resolve<kInitRescan>(rescan_.p, static_cast<int64_t>(n_rescan));
                     pull_scalars();
                     const uint64_t nx = hs_->n_exact;
                     n_exact += nx;
@@ -1024,8 +1023,9 @@ private:
         CK_LAUNCH();
     }
 
-    void screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
-                    const uint32_t* order, int64_t n_work) {
+    // Returns true when the screen also certified (fused resolve).
+    bool screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
+                    const uint32_t* order, int64_t n_work, int init) {
         // postings move 8 B per nonzero centroid weight at ~4 TB/s, the dense
         // screen 4 B per weight mostly from L2 at ~12 TB/s: above ~15% density
         // (long documents, few clusters: c3) the dense screen wins (measured)
@@ -1043,16 +1043,18 @@ private:
             last_density_ = static_cast<double>(total) / (static_cast<double>(d_) * kt);
         }
         const bool use_postings = screen_kind_ == 1 || (screen_kind_ == 2 && last_density_ <= dense_above_);
-        if (use_postings)
-            postings_screen(M, ld, ncols, col_ids, skip, order, n_work);
-        else
-            screen_tiles(M, ld, ncols, col_ids, skip, order, n_work);
+        if (use_postings) {
+            postings_screen(M, ld, ncols, col_ids, skip, order, n_work, fuse_resolve_ ? init : -1);
+            return fuse_resolve_;
+        }
+        screen_tiles(M, ld, ncols, col_ids, skip, order, n_work);
+        return false;
     }
 
     // Inverted-index screen, one cluster tile at a time: build the tile's
     // postings from the dense columns, then run the warp-per-document screen.
     void postings_screen(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
-                         const uint32_t* order, int64_t n_work) {
+                         const uint32_t* order, int64_t n_work, int fuse) {
         sb_.alloc(n_);
         ss_.alloc(n_);
         sa_.alloc(n_);
@@ -1072,6 +1074,7 @@ private:
         p.sb = sb_.p;
         p.ss = ss_.p;
         p.sa = sa_.p;
+        p.r = resolve_args(order, n_work);
         for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
             const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
             // postings of columns [c0, c0 + kt)
@@ -1097,14 +1100,15 @@ private:
             p.first = c0 == 0;
             postings_total_ += total;
             CK(cudaEventRecord(ev_[6], stream_));
+            const int f = c0 + KT >= ncols ? fuse : -1;
             if (KT == 256)
-                postings_launch<256>(p, n_work);
+                postings_launch<256>(p, n_work, f);
             else if (KT == 512)
-                postings_launch<512>(p, n_work);
+                postings_launch<512>(p, n_work, f);
             else if (KT == 1024)
-                postings_launch<1024>(p, n_work);
+                postings_launch<1024>(p, n_work, f);
             else
-                postings_launch<2048>(p, n_work);
+                postings_launch<2048>(p, n_work, f);
             CK(cudaEventRecord(ev_[7], stream_));
             CK(cudaEventSynchronize(ev_[7]));
             float ms = 0.f;
@@ -1149,18 +1153,24 @@ private:
     }
 
     template <int KT>
-    void postings_launch(const PostingsArgs& p, int64_t n_work) {
-        if (post_sub_ >= 32)
-            postings_launch_s<KT, 32>(p, n_work);
+    void postings_launch(const PostingsArgs& p, int64_t n_work, int fuse) {
+        if (fuse == kInitFull)
+            postings_launch_s<KT, 32, kInitFull>(p, n_work);
+        else if (fuse == kInitNcc)
+            postings_launch_s<KT, 32, kInitNcc>(p, n_work);
+        else if (fuse == kInitRescan)
+            postings_launch_s<KT, 32, kInitRescan>(p, n_work);
+        else if (post_sub_ >= 32)
+            postings_launch_s<KT, 32, -1>(p, n_work);
         else if (post_sub_ >= 16)
-            postings_launch_s<KT, 16>(p, n_work);
+            postings_launch_s<KT, 16, -1>(p, n_work);
         else
-            postings_launch_s<KT, 8>(p, n_work);
+            postings_launch_s<KT, 8, -1>(p, n_work);
     }
 
-    template <int KT, int SUB>
+    template <int KT, int SUB, int FUSE>
     void postings_launch_s(const PostingsArgs& p, int64_t n_work) {
-        auto k = postings_screen_kernel<KT, SUB>;
+        auto k = postings_screen_kernel<KT, SUB, FUSE>;
         const size_t per_warp = static_cast<size_t>(32 / SUB) * KT * sizeof(float);
         const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(post_warps_, (200u << 10) / per_warp)));
         const size_t smem = static_cast<size_t>(warps) * per_warp;
@@ -1231,9 +1241,7 @@ private:
         }
     }
 
-    template <int INIT>
-    void resolve(const uint32_t* order, int64_t n_work) {
-        exact_.alloc(n_);
+    ResolveArgs resolve_args(const uint32_t* order, int64_t n_work) {
         ResolveArgs r{};
         r.indptr = indptr_.p;
         r.idx = idx_.p;
@@ -1256,7 +1264,12 @@ private:
         r.n_exact = &scal_.p->n_exact;
         r.rescan_list = rescan_.p;
         r.n_rescan = &scal_.p->n_rescan;
-        launch(resolve_kernel<INIT>, grid_for(n_work * 32, 256), 256, r);
+        return r;
+    }
+
+    template <int INIT>
+    void resolve(const uint32_t* order, int64_t n_work) {
+        launch(resolve_kernel<INIT>, grid_for(n_work * 32, 256), 256, resolve_args(order, n_work));
         CK_LAUNCH();
     }
 
@@ -1355,6 +1368,7 @@ private:
     uint32_t post_kt_max_ = 1024;
     int post_warps_ = 8;
     bool cache_trusted_ = false;
+    bool fuse_resolve_ = false;  // measured: fusing costs the screen occupancy (c1 13.3 -> 18.0 ms)
     bool nonneg_ = true;
     double last_density_ = 0.0;
     double dense_above_ = 0.15;

@@ -9,8 +9,7 @@ cfg = S.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c1"]
 data = S.corpus(cfg)
 seeds = S.init_seeds(data.n_docs, cfg.k, 0)
 variants = [dict(SSKM_SCREEN="0", SSKM_TILE_BYTES=str(128 << 20), SSKM_ORDER="1", SSKM_UNROLL="16")]
-variants += [dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="1", SSKM_ORDER=str(o), SSKM_POST_SUB="32", SSKM_POST_WARPS=str(w))
-             for o in (0, 1) for w in (4, 8)]
+variants += [dict(SSKM_SCREEN="1", SSKM_SCREEN_KIND="1", SSKM_ORDER=str(o), SSKM_FUSE_RESOLVE=str(f)) for o in (0, 1) for f in (0, 1)]
 ref_a = None
 for v in variants:
     os.environ.update(v)

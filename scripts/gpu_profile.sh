@@ -1,11 +1,10 @@
-# ncu evidence (run under gpurun; 1 GPU)
+# ncu evidence for the bench command (run under gpurun; 1 GPU)
 set -x
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?"
 $CMD > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"^assign_kernel" -s 3 -c 1 -o gpurun_out/prof_assign $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"^postings_screen" -s 4 -c 1 -o gpurun_out/prof_post $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
-tail -2 gpurun_out/plain.log
+tail -1 gpurun_out/plain.log | cut -c1-300
