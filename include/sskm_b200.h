@@ -164,6 +164,10 @@ int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims,
                      sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters,
                      int32_t* stop_reason, double* objective);
 
+/* sskm_cluster_csr keeps one engine per device between calls (its HBM
+ * buffers are reused); this frees them. */
+int sskm_release_cache(void);
+
 /* ---- multi-GPU document sharding (one context per GPU / process) ----------
  * Documents are sharded in contiguous ranges; centroids and the fixed-point
  * cluster sums are replicated. An iteration's update exchanges only the rows

@@ -96,6 +96,7 @@ SIGNATURES = [
     ("sskm_cluster_csr", C.c_int, [_CFG, C.c_int64, C.c_uint32, _i64p, _i32p, _f32p, _P, _P, _P, _P,
                                    _ST, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_double)]),
+    ("sskm_release_cache", C.c_int, []),
     ("sskm_local_counts", C.c_int, [_P, _i64p]),
     ("sskm_local_candidates", C.c_int, [_P, C.c_int64, _f64p, _i64p, _u32p, C.POINTER(C.c_int64)]),
     ("sskm_move_doc", C.c_int, [_P, C.c_int64, C.c_uint32]),

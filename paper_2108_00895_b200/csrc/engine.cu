@@ -13,7 +13,9 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <string>
 #include <vector>
@@ -213,26 +215,26 @@ public:
         cfg_ = c;
         lambdas_.assign(c.lambdas, c.lambdas + c.n_lambdas);
         cfg_.lambdas = lambdas_.data();
-        if (k_ != c.k) {
-            k_ = c.k;
-            ld_ = static_cast<uint32_t>(round_up(k_, 128));
-            const uint64_t dk = static_cast<uint64_t>(d_) * ld_;
-            ct_.alloc(dk);
-            S_.alloc(dk);
-            unchanged_.alloc(k_);
-            touched_.alloc(k_);
-            repaired_flag_.alloc(k_);
-            counts_.alloc(k_);
-            rec_ids_.alloc(k_);
-            rec_pos_.alloc(k_);
-            chg_ids_.alloc(k_);
-            drift_.alloc(k_);
-            norm2_.alloc(k_);
-            drift_rec_.alloc(k_);
-            const uint64_t n_rb = ceil_div(d_, kRowBlock);
-            part_.alloc(n_rb * k_);
-            state_ = false;
-        }
+        // size every buffer for this (corpus, k); DevBuf::alloc only grows
+        k_ = c.k;
+        ld_ = static_cast<uint32_t>(round_up(k_, 128));
+        const uint64_t dk = static_cast<uint64_t>(d_) * ld_;
+        ct_.alloc(dk);
+        S_.alloc(dk);
+        unchanged_.alloc(k_);
+        touched_.alloc(k_);
+        repaired_flag_.alloc(k_);
+        counts_.alloc(k_);
+        rec_ids_.alloc(k_);
+        rec_pos_.alloc(k_);
+        chg_ids_.alloc(k_);
+        drift_.alloc(k_);
+        norm2_.alloc(k_);
+        drift_rec_.alloc(k_);
+        part_.alloc(ceil_div(d_, kRowBlock) * k_);
+        state_ = false;
+        have_cc_ = false;
+        cache_trusted_ = false;
         if (cfg_.mode != SSKM_MODE_BASELINE) cc_.alloc(static_cast<uint64_t>(d_) * ld_);
         obj_part_.alloc(kObjBlocks);
         prealloc();
@@ -1396,6 +1398,8 @@ struct sskm_ctx {
 
 namespace {
 thread_local std::string g_err;
+std::mutex g_cache_mu;
+std::map<int, std::unique_ptr<Engine>> g_engine_cache;
 
 template <class F>
 int guard(F&& f) {
@@ -1573,7 +1577,13 @@ int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims, 
     return guard([&] {
         if (!cfg) throw sskm_b200::InvalidArgument("null config");
         Engine::validate(*cfg, n_docs > 0 ? static_cast<uint64_t>(n_docs) : 0);
-        Engine e(cfg->device);
+        // one persistent engine per device: its HBM buffers are reused by the
+        // next call instead of being freed (cudaFree synchronises and costs
+        // ~0.1-0.5 s for the c1 working set)
+        std::lock_guard<std::mutex> lock(g_cache_mu);
+        auto& slot = g_engine_cache[cfg->device];
+        if (!slot) slot = std::make_unique<Engine>(cfg->device);
+        Engine& e = *slot;
         e.upload(n_docs, dims, indptr, indices, values, 0, n_docs);
         e.configure(*cfg);
         if (seeds) {
@@ -1597,6 +1607,13 @@ int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims, 
         if (n_iters) *n_iters = t;
         if (stop_reason) *stop_reason = reason;
         if (objective) *objective = obj;
+    });
+}
+
+int sskm_release_cache(void) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lock(g_cache_mu);
+        g_engine_cache.clear();
     });
 }
 

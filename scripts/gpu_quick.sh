@@ -1,2 +1,3 @@
 set -x
-timeout 2400 python -m pytest tests/test_gpu_parity.py -x -q -k large_sampled --durations=5 > gpurun_out/pytest_large.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_large.log
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; python -c "import json; d=json.loads(open('gpurun_out/bench.log').read().splitlines()[-1]); print(d['ms_per_step'], d['e2e'])"

@@ -321,3 +321,27 @@ def test_gpu_teacher_forced_large_sampled(cfg_name, iters, n_sample):
     seeds = S.init_seeds(m.n_docs, cfg.k, 0)
     sample = np.random.default_rng(1).choice(m.n_docs, n_sample, replace=False)
     teacher_forced(m, cfg.k, seeds, "ncc", iters, sample=sample, kind="port", n_cols=min(cfg.k, 200))
+
+
+def test_gpu_cluster_cached_engine_reshapes():
+    """cluster() reuses one engine per device: a larger vocabulary with the same
+    k, then a smaller corpus, must give the same results as fresh engines."""
+    import ctypes  # noqa: F401
+    from paper_2108_00895_b200 import _lib
+
+    small = S.generate(3000, 2048, 8, 40.0, seed=3)
+    big = S.generate(5000, 8192, 8, 40.0, seed=4)
+    out = []
+    for m in (small, big, small):
+        seeds = S.init_seeds(m.n_docs, 16, 0)
+        r = P.cluster(m, 16, mode="ncc", init_seeds=seeds, conv_sq_dist=1e-300, max_iters=8)
+        eng = engine_for(m, 16, mode="ncc", conv_sq_dist=1e-300, max_iters=8)
+        eng.init_from_seeds(seeds)
+        its, _ = eng.run()
+        a, s, _ = eng.get_state()
+        assert np.array_equal(r.assignments, a) and np.array_equal(r.sims, s)
+        assert np.array_equal(r.centroids, eng.get_centroids())
+        eng.close()
+        out.append(r.objective)
+    assert out[0] == out[2]
+    _lib.check(_lib.load().sskm_release_cache())
