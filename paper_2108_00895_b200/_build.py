@@ -22,7 +22,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O3",
     "-Xptxas", "-v",
     "-shared", "-cudart", "static",
-]
+] + [f for f in os.environ.get("SSKM_NVCC_EXTRA", "").split() if f]
 
 
 def _nvcc() -> str:

@@ -134,6 +134,15 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
+    override = os.environ.get("SSKM_LIB")  # experiments: load a specific build
+    if override:
+        lib = C.CDLL(override)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
     if _build.stale():
         try:
             _build.build()

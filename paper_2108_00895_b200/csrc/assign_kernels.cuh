@@ -362,6 +362,7 @@ struct ResolveArgs {
     const uint32_t* order;
     int64_t n_work;
     double cmax;               // upper bound on every centroid column's 2-norm
+    const double* xnorm2;      // per-document ||x||² (computed once at upload)
     int nonneg;                // all document weights > 0 (so centroids >= 0): relative bound
     const float* sb;
     const float* ss;
@@ -478,9 +479,19 @@ template <int INIT>
 __device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int64_t beg, int64_t end, int lane,
                                             float b, float s2, uint32_t sa);
 
+#ifndef SSKM_PAIR_L1
+#define SSKM_PAIR_L1 0
+#endif
+// Posting pairs bypass L1 (hit rate ~6%): L1TEX's SRAM is left to the
+// shared-memory accumulators the same warps update.
 __device__ __forceinline__ uint2 ld_pair(const uint2* p, uint64_t pol) {
     uint2 pr;
+#if SSKM_PAIR_L1
     asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(pr.x), "=r"(pr.y) : "l"(p), "l"(pol));
+#else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(pr.x), "=r"(pr.y) : "l"(p), "l"(pol));
+#endif
     return pr;
 }
 
@@ -672,14 +683,8 @@ __global__ void __launch_bounds__(256) postings_fill_kernel(const float* __restr
 template <int INIT>
 __device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int64_t beg, int64_t end, int lane,
                                             float b, float s2, uint32_t sa) {
-        // ||x||₂ (fp64) for the error bound
-        double q = 0.0;
-        for (int64_t e = beg + lane; e < end; e += kWarp) {
-            const double x = static_cast<double>(p.val[e]);
-            q = fma(x, x, q);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, off);
+        // ||x||₂ (fp64) for the error bound: precomputed per document
+        const double q = p.xnorm2[i];
         const double n = static_cast<double>(end - beg);
         const double u32 = 0x1p-24, u64 = 0x1p-53;
         const double n32 = n + 32.0;  // screen: any summation order, up to 32 partial sums
@@ -755,6 +760,24 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
     for (uint64_t w = gw; w < static_cast<uint64_t>(p.n_work); w += nw) {
         const int64_t i = p.order ? static_cast<int64_t>(p.order[w]) : static_cast<int64_t>(w);
         resolve_doc<INIT>(p, i, p.indptr[i], p.indptr[i + 1], lane, p.sb[i], p.ss[i], p.sa[i]);
+    }
+}
+
+// ||x_i||² per document (fp64), once per upload.
+__global__ void doc_norm2_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ val, int64_t n,
+                                 double* __restrict__ out) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
+    for (uint64_t i = gw; i < static_cast<uint64_t>(n); i += nw) {
+        double q = 0.0;
+        for (int64_t e = indptr[i] + lane; e < indptr[i + 1]; e += kWarp) {
+            const double x = static_cast<double>(val[e]);
+            q = fma(x, x, q);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, off);
+        if (lane == 0) out[i] = q;
     }
 }
 

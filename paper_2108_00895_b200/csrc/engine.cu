@@ -174,6 +174,9 @@ public:
         if (hs_->bad & 8u)
             throw InvalidArgument("document weights must be finite with |x| <= 1 (unit-length rows)");
         nonneg_ = (hs_->bad & 16u) == 0;
+        xnorm2_.alloc(n);
+        launch(doc_norm2_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p);
+        CK_LAUNCH();
         // fixed-point scale: N_total · 2^K <= 2^62 with |x| <= 1
         int lg = 0;
         while ((int64_t(1) << lg) < n_total_) ++lg;
@@ -1253,6 +1256,7 @@ private:
         r.order = order;
         r.n_work = n_work;
         r.cmax = cmax_;
+        r.xnorm2 = xnorm2_.p;
         r.nonneg = nonneg_ ? 1 : 0;
         r.sb = sb_.p;
         r.ss = ss_.p;
@@ -1357,7 +1361,7 @@ private:
     DevBuf<float> ct_, cc_;
     DevBuf<long long> S_;
     DevBuf<uint32_t> a_, a_sum_, a_start_, moved_, rescan_, rec_ids_, rec_pos_, chg_ids_;
-    DevBuf<double> sims_start_;
+    DevBuf<double> sims_start_, xnorm2_;
     DevBuf<float> sb_, ss_;
     DevBuf<uint32_t> pcnt_, pptr_;
     DevBuf<uint2> pairs_;
