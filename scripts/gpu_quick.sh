@@ -1,6 +1,3 @@
 set -x
-for lib in paper_2108_00895_b200/libsskm_b200.so paper_2108_00895_b200/libsskm_b200_l1.so; do
-  SSKM_LIB=$PWD/$lib timeout 600 python scripts/configs_probe.py c1 baseline 5 > gpurun_out/p.log 2>&1; echo "$lib rc=$?"; tail -1 gpurun_out/p.log | cut -c1-120
-  SSKM_LIB=$PWD/$lib timeout 600 python scripts/configs_probe.py c4 baseline 1 > gpurun_out/p4.log 2>&1; echo "$lib c4 rc=$?"; tail -1 gpurun_out/p4.log | cut -c1-120
-done
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -k "approximate or teacher_forced_c0" > gpurun_out/pytest_eps.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_eps.log
+timeout 900 python scripts/configs_probe.py c2 ncc 14 > gpurun_out/c2ncc.log 2>&1; echo "c2 rc=$?"; grep iter gpurun_out/c2ncc.log | cut -c1-260

@@ -179,15 +179,15 @@ def centroid_rel_err(ct, ptr, idx, val, cols=None):
     return worst_rel, worst_abs
 
 
-def teacher_forced(m, k, seeds, mode, iters, sample=None, kind="port", n_cols=None):
+def teacher_forced(m, k, seeds, mode, iters, sample=None, kind="port", n_cols=None, ncc_epsilon=0.0):
     """Run the GPU; at every iteration feed its state/centroids to the oracle."""
-    eng = engine_for(m, k, mode=mode, conv_sq_dist=1e-300, max_iters=iters)
+    eng = engine_for(m, k, mode=mode, conv_sq_dist=1e-300, max_iters=iters, ncc_epsilon=ncc_epsilon)
     eng.init_from_seeds(seeds)
     docs = np.arange(m.n_docs) if sample is None else np.sort(sample)
     c_full = ref_corpus(m)
     c_samp = c_full if sample is None else ref_corpus(m, docs)
-    upd = O.Stepper(c_full, k, mode, kind=kind)
-    asg = upd if sample is None else O.Stepper(c_samp, min(k, c_samp.n), mode, kind=kind)
+    upd = O.Stepper(c_full, k, mode, kind=kind, ncc_epsilon=ncc_epsilon)
+    asg = upd if sample is None else O.Stepper(c_samp, min(k, c_samp.n), mode, kind=kind, ncc_epsilon=ncc_epsilon)
     if sample is not None:
         assert k <= c_samp.n
     report = []
@@ -230,6 +230,16 @@ def test_gpu_teacher_forced_c0(mode):
     seeds = S.init_seeds(m.n_docs, cfg.k, 0)
     rep = teacher_forced(m, cfg.k, seeds, mode, cfg.iterations)
     assert len(rep) == cfg.iterations
+
+
+def test_gpu_teacher_forced_approximate_ncc():
+    """ncc_epsilon > 0: centroids that moved by less than epsilon
+    are treated as unchanged; the GPU must follow the reference's NCC literally
+    (no full-scan shortcut) and still match it bitwise given the same state."""
+    m = S.generate(8000, 4096, 20, 60.0, seed=8)
+    seeds = S.init_seeds(m.n_docs, 40, 0)
+    rep = teacher_forced(m, 40, seeds, "ncc", 10, ncc_epsilon=2e-3)
+    assert len(rep) == 10
 
 
 def test_gpu_modes_bitwise_equivalent_c0():
