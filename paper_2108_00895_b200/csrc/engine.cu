@@ -82,11 +82,8 @@ public:
         sms_ = prop.multiProcessorCount;
         if (const char* e = std::getenv("SSKM_TILE_BYTES")) tile_bytes_ = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("SSKM_ORDER")) order_enabled_ = std::atoi(e) != 0;
-        if (const char* e = std::getenv("SSKM_UNROLL")) unroll_ = std::atoi(e);
-        if (const char* e = std::getenv("SSKM_SCREEN_UNROLL")) screen_unroll_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
-        if (const char* e = std::getenv("SSKM_POST_SUB")) post_sub_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_POST_KT")) post_kt_max_ = static_cast<uint32_t>(std::atoi(e));
         if (const char* e = std::getenv("SSKM_POST_WARPS")) post_warps_ = std::max(1, std::min(8, std::atoi(e)));
         if (const char* e = std::getenv("SSKM_DENSE_ABOVE")) dense_above_ = std::atof(e);
@@ -100,8 +97,7 @@ public:
         scal_.alloc(1);
         CK(cudaMallocHost(&hs_, sizeof(Scalars)));
         // the screen keeps hot Cᵀ rows in L1: give L1 the whole carveout
-        for (auto k : {screen_tile_kernel<1, 8>, screen_tile_kernel<2, 8>, screen_tile_kernel<4, 8>,
-                       screen_tile_kernel<1, 16>, screen_tile_kernel<2, 16>, screen_tile_kernel<4, 16>})
+        for (auto k : {screen_tile_kernel<1, 16>, screen_tile_kernel<2, 16>, screen_tile_kernel<4, 16>})
             CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     }
 
@@ -797,19 +793,6 @@ private:
         CK_LAUNCH();
     }
 
-    uint64_t find_donor() {
-        // requires counts_ to hold the (global) cluster sizes
-        CK(cudaMemsetAsync(&scal_.p->donor_key, 0xFF, 8, stream_));
-        CK(cudaMemsetAsync(&scal_.p->donor_idx, 0xFF, 8, stream_));
-        launch(donor_sim_kernel, grid_for(n_, 256), 256, a_.p, sims_.p, n_, counts_.p,
-                                                                 &scal_.p->donor_key);
-        launch(donor_idx_kernel, grid_for(n_, 256), 256, a_.p, sims_.p, n_, counts_.p,
-                                                                 &scal_.p->donor_key, &scal_.p->donor_idx);
-        CK_LAUNCH();
-        pull_scalars();
-        return hs_->donor_idx;
-    }
-
     // Empty-cluster repair for one context (engine.cpp:154-167): ascending
     // empty clusters, each taking the lowest-(sim, index) document among those
     // whose cluster can spare one. One stable radix sort of (sim, doc) keys
@@ -1165,12 +1148,8 @@ private:
             postings_launch_s<KT, 32, kInitNcc>(p, n_work);
         else if (fuse == kInitRescan)
             postings_launch_s<KT, 32, kInitRescan>(p, n_work);
-        else if (post_sub_ >= 32)
-            postings_launch_s<KT, 32, -1>(p, n_work);
-        else if (post_sub_ >= 16)
-            postings_launch_s<KT, 16, -1>(p, n_work);
         else
-            postings_launch_s<KT, 8, -1>(p, n_work);
+            postings_launch_s<KT, 32, -1>(p, n_work);  // split-warp lists (SUB < 32) measured slower: not built
     }
 
     template <int KT, int SUB, int FUSE>
@@ -1237,13 +1216,8 @@ private:
 
     template <int V>
     void screen_launch(const ScreenArgs& p, int64_t n_work) {
-        if (screen_unroll_ >= 16) {
-            auto k = screen_tile_kernel<V, 16>;
-            launch(k, resident_grid(k, n_work), 256, p);
-        } else {
-            auto k = screen_tile_kernel<V, 8>;
-            launch(k, resident_grid(k, n_work), 256, p);
-        }
+        auto k = screen_tile_kernel<V, 16>;
+        launch(k, resident_grid(k, n_work), 256, p);
     }
 
     ResolveArgs resolve_args(const uint32_t* order, int64_t n_work) {
@@ -1291,12 +1265,7 @@ private:
 
     template <int INIT>
     void launch_tile(int v, unsigned grid, const TileArgs& p) {
-        if (unroll_ >= 16)
-            launch_tile_u<INIT, 16>(v, grid, p);
-        else if (unroll_ >= 8)
-            launch_tile_u<INIT, 8>(v, grid, p);
-        else
-            launch_tile_u<INIT, 4>(v, grid, p);
+        launch_tile_u<INIT, 16>(v, grid, p);
     }
 
     void finish_assign(sskm_iteration_stats* st) {
@@ -1337,9 +1306,7 @@ private:
     uint64_t tile_bytes_ = 64ull << 20;
     bool order_enabled_ = true;
     int blocks_per_sm_ = 2;
-    int unroll_ = 16;
     int screen_blocks_per_sm_ = 8;
-    int screen_unroll_ = 16;
     bool screen_enabled_ = true;
     double cmax_ = 1.0;
     DevBuf<Scalars> scal_;
@@ -1370,7 +1337,6 @@ private:
     double screen_ms_ = 0.0;
     uint32_t screen_launches_ = 0;
     int screen_kind_ = 2;  // 0 dense, 1 postings, 2 by measured density
-    int post_sub_ = 32;
     uint32_t post_kt_max_ = 1024;
     int post_warps_ = 8;
     bool cache_trusted_ = false;

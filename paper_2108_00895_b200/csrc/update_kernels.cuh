@@ -37,30 +37,6 @@ __global__ void count_empty_kernel(const unsigned long long* __restrict__ counts
         if (counts[j] == 0) atomicAdd(n_empty, 1u);
 }
 
-// Donor for empty-cluster repair (engine.cpp:156-161): lowest cached sim among
-// documents in clusters of size >= 2, ties to the lowest document index. Two
-// order-independent atomicMin passes give the reference's sequential answer.
-__global__ void donor_sim_kernel(const uint32_t* __restrict__ a, const double* __restrict__ sims,
-                                 int64_t n, const unsigned long long* __restrict__ counts,
-                                 unsigned long long* key) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        if (counts[a[i]] < 2) continue;
-        atomicMin(key, orderable(sims[i]));
-    }
-}
-
-__global__ void donor_idx_kernel(const uint32_t* __restrict__ a, const double* __restrict__ sims,
-                                 int64_t n, const unsigned long long* __restrict__ counts,
-                                 const unsigned long long* key, unsigned long long* idx_out) {
-    const unsigned long long kk = *key;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        if (counts[a[i]] < 2) continue;
-        if (orderable(sims[i]) == kk) atomicMin(idx_out, static_cast<unsigned long long>(i));
-    }
-}
-
 // Documents whose cluster differs from the cluster their row is summed into.
 __global__ void moved_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ a_sum,
                              int64_t n, uint32_t* __restrict__ moved,
