@@ -127,6 +127,13 @@ def _load(kind: str):
         lib.sref_seed_kmeanspp.argtypes = [_P, C.c_uint32, C.c_uint64, C.c_uint32, _u32p, _u32p, _f64p]
         lib.sref_validate.argtypes = [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
                                       _f64p, C.c_uint32]
+        lib.sref_load_matrix.restype = _P
+        lib.sref_load_matrix.argtypes = [C.c_char_p]
+        lib.sref_write_matrix.argtypes = [C.c_char_p, _P]
+        lib.sref_report_json.argtypes = [C.c_uint32, C.c_char_p, _f64p, C.c_uint32, C.c_double, C.c_double,
+                                         C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32,
+                                         C.POINTER(CStats), C.c_uint32, C.c_double, C.c_int32, _u32p,
+                                         C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
     else:
         lib.o_last_error.restype = C.c_char_p
         lib.o_dot.restype = C.c_double
@@ -475,3 +482,49 @@ def seed_kmeanspp(corpus: Corpus, k, seed, threads=0):
     sm = np.zeros(corpus.n, np.float64)
     _check(lib, lib.sref_seed_kmeanspp(corpus.ref_handle(), k, seed, threads, seeds, a, sm), "ref")
     return seeds, a, sm
+
+
+# ------------------------------------------------------------- corpus IO ----
+def ref_load_matrix(path):
+    """The reference's load_matrix (corpus.cpp:201-272) -> (indptr, idx, val f64, dims, n)."""
+    lib = _load("ref")
+    h = lib.sref_load_matrix(path.encode())
+    if not h:
+        raise OracleError(lib.sref_last_error().decode())
+    try:
+        n = lib.sref_corpus_n(h)
+        nnz = lib.sref_corpus_nnz(h)
+        ptr = np.zeros(n + 1, np.int64)
+        idx = np.zeros(max(nnz, 1), np.uint32)
+        val = np.zeros(max(nnz, 1), np.float64)
+        lib.sref_corpus_export(h, ptr, idx, val)
+        return ptr, idx[:nnz].astype(np.int32), val[:nnz], int(lib.sref_corpus_dims(h))
+    finally:
+        lib.sref_corpus_free(h)
+
+
+def ref_write_matrix(path, corpus: Corpus):
+    """The reference's write_matrix (corpus.cpp:182-199) of a CSR corpus."""
+    lib = _load("ref")
+    _check(lib, lib.sref_write_matrix(path.encode(), corpus.ref_handle()), "ref")
+
+
+def ref_report_json(cfg: dict, n_docs, dims, iterations, objective, stop_reason, assignments) -> str:
+    """The reference's to_json(make_report(...)) (report.cpp:10-79)."""
+    lib = _load("ref")
+    its = (CStats * max(len(iterations), 1))()
+    for t, it in enumerate(iterations):
+        for f, _ in CStats._fields_:
+            if f in it:
+                setattr(its[t], f, it[f])
+    lam = np.ascontiguousarray(cfg.get("lambdas", [0.1, 0.25, 0.4, 0.6]), np.float64)
+    a = np.ascontiguousarray(assignments, np.uint32)
+    n = C.c_uint64()
+    args = [cfg["k"], cfg.get("mode", "baseline").encode(), lam if len(lam) else np.zeros(1), len(lam),
+            cfg.get("conv_sq_dist", 1e-4), cfg.get("ncc_epsilon", 0.0), cfg.get("index_activation_threshold", 100),
+            cfg.get("max_iters", 100), cfg.get("seed", 0), cfg.get("threads", 0), n_docs, dims, its, len(iterations),
+            objective, STOP_REASONS.index(stop_reason), a]
+    _check(lib, lib.sref_report_json(*args, None, 0, C.byref(n)), "ref")
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib, lib.sref_report_json(*args, buf, n.value + 1, C.byref(n)), "ref")
+    return buf.value.decode()

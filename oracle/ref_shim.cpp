@@ -29,6 +29,7 @@
 #include "sskm/corpus.hpp"
 #include "sskm/engine.hpp"
 #include "sskm/prune_index.hpp"
+#include "sskm/report.hpp"
 #include "sskm/sparse_vector.hpp"
 #include "sskm/synthetic.hpp"
 
@@ -472,6 +473,63 @@ int sref_seed_kmeanspp(void* corpus, std::uint32_t k, std::uint64_t seed, std::u
         std::memcpy(seeds, r.seeds.data(), r.seeds.size() * 4);
         std::memcpy(assignments, r.assignments.data(), r.assignments.size() * 4);
         std::memcpy(sims, r.sims.data(), r.sims.size() * 8);
+    });
+}
+
+// ---------------------------------------------------------- corpus IO ---
+// load_matrix / write_matrix (corpus.cpp:182-272) and the run report JSON
+// (report.cpp:24-79), for IO / report parity tests.
+void* sref_load_matrix(const char* path) {
+    CorpusMatrix* m = nullptr;
+    int rc = guard([&] { m = new CorpusMatrix(load_matrix(path)); });
+    return rc == 0 ? m : nullptr;
+}
+
+int sref_write_matrix(const char* path, void* corpus) {
+    return guard([&] { write_matrix(path, *static_cast<CorpusMatrix*>(corpus)); });
+}
+
+// RunReport JSON for a result described by plain arrays.
+int sref_report_json(std::uint32_t k, const char* mode, const double* lambdas, std::uint32_t n_lambdas,
+                     double conv_sq_dist, double ncc_epsilon, std::uint32_t iat, std::uint32_t max_iters,
+                     std::uint64_t seed, std::uint32_t threads, std::uint64_t n_docs, std::uint32_t dims,
+                     const CStats* its, std::uint32_t n_it, double objective, std::int32_t stop,
+                     const std::uint32_t* assignments, char* out, std::uint64_t cap, std::uint64_t* len) {
+    return guard([&] {
+        RunReport r;
+        r.config.k = k;
+        r.config.mode = parse_mode(mode);
+        r.config.lambdas.assign(lambdas, lambdas + n_lambdas);
+        r.config.conv_sq_dist = conv_sq_dist;
+        r.config.ncc_epsilon = ncc_epsilon;
+        r.config.index_activation_threshold = iat;
+        r.config.max_iters = max_iters;
+        r.config.seed = seed;
+        r.config.threads = threads;
+        r.n_docs = n_docs;
+        r.dims = dims;
+        for (std::uint32_t t = 0; t < n_it; ++t) {
+            IterationStats s;
+            s.iteration = its[t].iteration;
+            s.n_reassigned = its[t].n_reassigned;
+            s.n_unchanged_centroids = its[t].n_unchanged_centroids;
+            s.dot_products = its[t].dot_products;
+            s.index_queries = its[t].index_queries;
+            s.candidates_total = its[t].candidates_total;
+            s.wall_seconds = its[t].wall_seconds;
+            s.index_build_seconds = its[t].index_build_seconds;
+            s.index_active = its[t].index_active != 0;
+            s.max_sq_drift = its[t].max_sq_drift;
+            s.objective = its[t].objective;
+            r.iterations.push_back(s);
+        }
+        r.objective = objective;
+        r.stop_reason = static_cast<StopReason>(stop);
+        r.cluster_sizes.assign(k, 0);
+        for (std::uint64_t i = 0; i < n_docs; ++i) ++r.cluster_sizes[assignments[i]];
+        const std::string j = to_json(r);
+        *len = j.size();
+        if (out && cap > j.size()) std::memcpy(out, j.c_str(), j.size() + 1);
     });
 }
 

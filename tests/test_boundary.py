@@ -15,7 +15,7 @@ from tests.conftest import ROOT, gpu_available
 
 def header_symbols():
     syms = set()
-    for h in ["sskm_b200.h", "sskm_synth.h"]:
+    for h in ["sskm_b200.h", "sskm_synth.h", "sskm_io.h"]:
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         syms |= set(re.findall(r"\b(sskm_[a-z0-9_]+)\s*\(", src))
@@ -32,7 +32,11 @@ def test_exports_every_header_symbol():
     missing = [s for s in sorted(header_symbols()) if not hasattr(lib, s)]
     assert not missing, missing
     bound = {name for name, _, _ in _lib.SIGNATURES}
-    assert header_symbols() <= bound, header_symbols() - bound
+    from paper_2108_00895_b200 import io as IO
+
+    IO._io()
+    io_bound = {s for s in header_symbols() if s.startswith("sskm_io_") and getattr(lib, s, None) is not None}
+    assert header_symbols() <= bound | io_bound, header_symbols() - bound - io_bound
 
 
 def test_validate_matches_reference_messages():
