@@ -501,6 +501,18 @@ __device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int
 #endif
 // Posting pairs bypass L1 (hit rate ~6%): L1TEX's SRAM is left to the
 // shared-memory accumulators the same warps update.
+// Shared-memory accumulator access through a 32-bit shared address computed
+// once per warp (a generic pointer makes ptxas rebuild the shared window base
+// on every access inside the predicated loop).
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v));
+}
+
 __device__ __forceinline__ uint2 ld_pair(const uint2* p, uint64_t pol) {
     uint2 pr;
 #if SSKM_PAIR_L1
@@ -526,6 +538,8 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
     const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
     float* accw = smem_acc + static_cast<size_t>(warp) * G * KT;
     float* accg = accw + grp * KT;
+    const uint32_t acc_s = static_cast<uint32_t>(__cvta_generic_to_shared(accg));
+    const uint2* __restrict__ pairs = p.pairs;
     const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_work, gridDim.x));
     const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
     const int64_t w1 = imin64(p.n_work, w0 + chunk);
@@ -554,19 +568,24 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
                 // while the current term accumulates (hides one L2 round trip)
                 uint32_t qb = __shfl_sync(0xFFFFFFFFu, lb, 0) + lane, qe = __shfl_sync(0xFFFFFFFFu, le, 0);
                 float x = __shfl_sync(0xFFFFFFFFu, x_l, 0);
-                uint2 pr = qb < qe ? ld_pair(p.pairs + qb, pol_keep) : make_uint2(0u, 0u);
+                uint2 pr = qb < qe ? ld_pair(pairs + qb, pol_keep) : make_uint2(0u, 0u);
                 for (int j = 0; j < n; ++j) {
                     const int jn = (j + 1) & (kWarp - 1);
-                    uint32_t nb = __shfl_sync(0xFFFFFFFFu, lb, jn) + lane, ne = __shfl_sync(0xFFFFFFFFu, le, jn);
+                    const uint32_t nb = __shfl_sync(0xFFFFFFFFu, lb, jn) + lane;
+                    uint32_t ne = __shfl_sync(0xFFFFFFFFu, le, jn);
                     const float nx = __shfl_sync(0xFFFFFFFFu, x_l, jn);
-                    if (j + 1 >= n) ne = 0;
-                    const uint2 npr = nb < ne ? ld_pair(p.pairs + nb, pol_keep) : make_uint2(0u, 0u);
-                    if (qb < qe) accg[pr.x] = fmaf(x, __uint_as_float(pr.y), accg[pr.x]);
+                    ne = j + 1 < n ? ne : 0u;
+                    const uint2 npr = nb < ne ? ld_pair(pairs + nb, pol_keep) : make_uint2(0u, 0u);
+                    if (qb < qe) {
+                        const uint32_t a = acc_s + pr.x * 4u;
+                        sts_f32(a, fmaf(x, __uint_as_float(pr.y), lds_f32(a)));
+                    }
                     // most lists fit the prefetched first 32; keep the rare tail compact
 #pragma unroll 1
                     for (uint32_t q = qb + kWarp; q < qe; q += kWarp) {
-                        const uint2 t2 = ld_pair(p.pairs + q, pol_keep);
-                        accg[t2.x] = fmaf(x, __uint_as_float(t2.y), accg[t2.x]);
+                        const uint2 t2 = ld_pair(pairs + q, pol_keep);
+                        const uint32_t a = acc_s + t2.x * 4u;
+                        sts_f32(a, fmaf(x, __uint_as_float(t2.y), lds_f32(a)));
                     }
                     __syncwarp();
                     qb = nb;
@@ -591,13 +610,23 @@ __global__ void __launch_bounds__(256) postings_screen_kernel(PostingsArgs p) {
         // combine the G partial accumulators (fixed order), then top-2
         float tb = -INFINITY, ts2 = -INFINITY;
         uint32_t ta = kNone;
-        for (int c = lane; c < static_cast<int>(p.kt); c += kWarp) {
-            float v = accw[c];
+        const uint32_t accw_s = static_cast<uint32_t>(__cvta_generic_to_shared(accw));
+        if (p.col_ids) {
+            for (int c = lane; c < static_cast<int>(p.kt); c += kWarp) {
+                float v = lds_f32(accw_s + 4u * c);
 #pragma unroll
-            for (int g = 1; g < G; ++g) v += accw[g * KT + c];
-            const uint32_t col = p.c0 + static_cast<uint32_t>(c);
-            const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
-            if (id != skip) top2_push(v, id, tb, ta, ts2);
+                for (int g = 1; g < G; ++g) v += lds_f32(accw_s + 4u * (g * KT + c));
+                const uint32_t id = __ldg(p.col_ids + p.c0 + static_cast<uint32_t>(c));
+                if (id != skip) top2_push(v, id, tb, ta, ts2);
+            }
+        } else {
+            for (int c = lane; c < static_cast<int>(p.kt); c += kWarp) {
+                float v = lds_f32(accw_s + 4u * c);
+#pragma unroll
+                for (int g = 1; g < G; ++g) v += lds_f32(accw_s + 4u * (g * KT + c));
+                const uint32_t id = p.c0 + static_cast<uint32_t>(c);
+                if (id != skip) top2_push(v, id, tb, ta, ts2);
+            }
         }
         warp_top2(tb, ta, ts2);
         float b = -INFINITY, s2 = -INFINITY;
