@@ -142,6 +142,65 @@ __device__ __forceinline__ double doc_col_dot(const int32_t* __restrict__ idx,
     return s;
 }
 
+// doc_col_dot with the fold through a per-warp shared buffer: the lanes form
+// the exact fp64 products x_t*c_t in parallel (fp32 x fp32 is exact in fp64, so
+// s + p_t is bit-identical to fma(x_t, c_t, s)), then every lane folds them in
+// ascending term order from broadcast 16-byte shared loads.
+__device__ __forceinline__ double doc_col_dot_sm(const int32_t* __restrict__ idx,
+                                                 const float* __restrict__ val, int64_t beg,
+                                                 int64_t end, const float* __restrict__ M,
+                                                 uint64_t ld, uint32_t col, int lane, double* wsm) {
+    constexpr int kChunks = 4;
+    double s = 0.0;
+    for (int64_t e0 = beg; e0 < end; e0 += kChunks * kWarp) {
+        float xs[kChunks];
+        int32_t ts[kChunks];
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) {
+            const int64_t e = e0 + c * kWarp + lane;
+            xs[c] = 0.f;
+            ts[c] = -1;
+            if (e < end) {
+                ts[c] = __ldg(idx + e);
+                xs[c] = __ldg(val + e);
+            }
+        }
+        double ps[kChunks];
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) {
+            const float cv = ts[c] >= 0 ? __ldg(M + static_cast<uint64_t>(ts[c]) * ld + col) : 0.f;
+            ps[c] = static_cast<double>(xs[c]) * static_cast<double>(cv);
+        }
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) {
+            const int64_t c0 = e0 + c * kWarp;
+            if (c0 >= end) break;
+            const int n = static_cast<int>(imin64(kWarp, end - c0));
+            wsm[lane] = ps[c];
+            __syncwarp();
+            const double2* w2 = reinterpret_cast<const double2*>(wsm);
+            if (n == kWarp) {
+#pragma unroll
+                for (int j = 0; j < kWarp / 2; ++j) {
+                    const double2 q = w2[j];
+                    s += q.x;
+                    s += q.y;
+                }
+            } else {
+                int j = 0;
+                for (; j + 2 <= n; j += 2) {
+                    const double2 q = w2[j >> 1];
+                    s += q.x;
+                    s += q.y;
+                }
+                if (j < n) s += wsm[j];
+            }
+            __syncwarp();
+        }
+    }
+    return s;
+}
+
 enum ScanInit : int {
     kInitFull = 0,    // best = -2, arg = 0 (engine.cpp:252-253), all columns
     kInitNcc = 1,     // NCC pass A: cache or refreshed own dot, changed columns only
@@ -492,9 +551,9 @@ struct PostingsArgs {
     ResolveArgs r;             // used when the last tile certifies in place (FUSE >= 0)
 };
 
-template <int INIT>
+template <int INIT, bool SM = false>
 __device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int64_t beg, int64_t end, int lane,
-                                            float b, float s2, uint32_t sa);
+                                            float b, float s2, uint32_t sa, double* wsm = nullptr);
 
 #ifndef SSKM_PAIR_L1
 #define SSKM_PAIR_L1 0
@@ -726,9 +785,14 @@ __global__ void __launch_bounds__(256) postings_fill_kernel(const float* __restr
 // Certify one document's screen result (b, s2, sa) and write the exact answer
 // (or queue the document for the exact scan). Called by resolve_kernel and,
 // fused, by the screen kernels on their last cluster tile.
-template <int INIT>
+template <int INIT, bool SM>
 __device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int64_t beg, int64_t end, int lane,
-                                            float b, float s2, uint32_t sa) {
+                                            float b, float s2, uint32_t sa, double* wsm) {
+        // SM: the caller provides a 32-double per-warp buffer for the fold
+        auto dot = [&](uint32_t col) {
+            if constexpr (SM) return doc_col_dot_sm(p.idx, p.val, beg, end, p.CT, p.ld_ct, col, lane, wsm);
+            else return doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, col, lane);
+        };
         // ||x||₂ (fp64) for the error bound: precomputed per document
         const double q = p.xnorm2[i];
         const double n = static_cast<double>(end - beg);
@@ -757,7 +821,7 @@ __device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int
             best = 0.0;
             arg = sa;
             if (certain) {
-                best = doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, sa, lane);
+                best = dot(sa);
                 certain = best > -2.0;
             }
         } else {
@@ -766,14 +830,14 @@ __device__ __forceinline__ void resolve_doc(const ResolveArgs& p, int64_t i, int
             const uint32_t a0 = INIT == kInitRescan ? p.a[i] : p.a_start[i];
             old_sim = INIT == kInitRescan ? p.sims[i] : p.sims_start[i];
             own_changed = INIT == kInitNcc && p.unchanged[a0] == 0;
-            const double sim0 = own_changed ? doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, a0, lane)
+            const double sim0 = own_changed ? dot(a0)
                                             : old_sim;
             best = sim0;
             arg = a0;
             if (sa == kNone || upper(bd) < sim0) {
                 certain = true;  // no screened column can reach the baseline
             } else if (lower(bd) > sim0 && lower(bd) > upper(s2d)) {
-                best = doc_col_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, sa, lane);
+                best = dot(sa);
                 arg = sa;
                 certain = true;
             } else {
@@ -803,9 +867,31 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
-    for (uint64_t w = gw; w < static_cast<uint64_t>(p.n_work); w += nw) {
-        const int64_t i = p.order ? static_cast<int64_t>(p.order[w]) : static_cast<int64_t>(w);
-        resolve_doc<INIT>(p, i, p.indptr[i], p.indptr[i + 1], lane, p.sb[i], p.ss[i], p.sa[i]);
+    __shared__ __align__(16) double fold[256];
+    double* wsm = fold + (threadIdx.x & ~(kWarp - 1));
+    // software pipeline: the next document's id, extent and screen result are
+    // loaded while the current one is resolved
+    const uint64_t n_work = static_cast<uint64_t>(p.n_work);
+    auto fetch = [&](uint64_t w, int64_t& i, int64_t& beg, int64_t& end, float& b, float& s2, uint32_t& sa) {
+        i = p.order ? static_cast<int64_t>(__ldg(p.order + w)) : static_cast<int64_t>(w);
+        beg = __ldg(p.indptr + i);
+        end = __ldg(p.indptr + i + 1);
+        b = __ldg(p.sb + i);
+        s2 = __ldg(p.ss + i);
+        sa = __ldg(p.sa + i);
+    };
+    if (gw >= n_work) return;
+    int64_t i, beg, end;
+    float b, s2;
+    uint32_t sa;
+    fetch(gw, i, beg, end, b, s2, sa);
+    for (uint64_t w = gw; w < n_work; w += nw) {
+        int64_t ni = 0, nbeg = 0, nend = 0;
+        float nb = 0.f, ns2 = 0.f;
+        uint32_t nsa = 0;
+        if (w + nw < n_work) fetch(w + nw, ni, nbeg, nend, nb, ns2, nsa);
+        resolve_doc<INIT, true>(p, i, beg, end, lane, b, s2, sa, wsm);
+        i = ni, beg = nbeg, end = nend, b = nb, s2 = ns2, sa = nsa;
     }
 }
 
