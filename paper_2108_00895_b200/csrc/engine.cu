@@ -25,6 +25,7 @@
 #include "../../include/sskm_b200.h"
 #include "assign_kernels.cuh"
 #include "common.cuh"
+#include "index_kernels.cuh"
 #include "update_kernels.cuh"
 
 namespace sskm_b200 {
@@ -410,12 +411,204 @@ public:
         need_state();
         const bool full = iteration_ <= 1 || cfg_.mode == SSKM_MODE_BASELINE;
         st->iteration = iteration_;
+        st->index_active = 0;
+        st->index_queries = 0;
+        st->candidates_total = 0;
+        st->index_build_seconds = 0.0;
         if (full) {
             full_assign(st);
         } else {
             ncc_assign(st);
+            // engine.cpp:384-386: the reference builds its Lemma-1 index when
+            // more than index_activation_threshold centroids changed
+            if (cfg_.mode == SSKM_MODE_NCC_INDEX && n_chg_ > cfg_.index_activation_threshold && cfg_.n_lambdas > 0)
+                index_account(st);
         }
-        st->index_active = 0;
+    }
+
+    // ---------------------------------------------------------- ncc+index --
+    // Buffers whose size follows the centroids grow with headroom, so the
+    // iteration-to-iteration drift does not reallocate every time.
+    template <typename T>
+    static void grow(DevBuf<T>& b, size_t count) {
+        if (count > b.n) b.alloc(count + count / 4);
+    }
+
+    // The reference's Lemma-1 index over the current centroids and its queries
+    // (index_kernels.cuh), replayed after the exact NCC assign to report the
+    // reference's index_queries, candidates_total and dot_products.
+    void index_account(sskm_iteration_stats* st) {
+        const uint32_t L = cfg_.n_lambdas;
+        CK(cudaEventRecord(ev_[6], stream_));
+        // 1. supports, (|w| desc, term asc) per centroid
+        const int64_t want = static_cast<int64_t>(sms_) * 2048;
+        uint32_t nch = static_cast<uint32_t>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, k_), d_ / 16 + 1)));
+        const uint32_t rows = static_cast<uint32_t>(ceil_div(d_, nch));
+        nch = static_cast<uint32_t>(ceil_div(d_, rows));
+        const uint64_t ncnt = static_cast<uint64_t>(k_) * nch;
+        ix_cnt_.alloc(ncnt + 1);
+        ix_off_.alloc(ncnt + 1);
+        CK(cudaMemsetAsync(ix_cnt_.p + ncnt, 0, 4, stream_));
+        const dim3 g2(static_cast<unsigned>(ceil_div(k_, 128)), nch);
+        idx_support_count_kernel<<<g2, 128, 0, stream_>>>(ct_.p, ld_, d_, k_, rows, nch, ix_cnt_.p);
+        ++launches_;
+        CK_LAUNCH();
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ix_cnt_.p, ix_off_.p, static_cast<int>(ncnt + 1), stream_));
+        grow(ix_tmp_, tmp);
+        CK(cub::DeviceScan::ExclusiveSum(ix_tmp_.p, tmp, ix_cnt_.p, ix_off_.p, static_cast<int>(ncnt + 1), stream_));
+        ++launches_;
+        ix_cptr_.alloc(k_ + 1);
+        // cluster c starts at off[c * nch]; the total is off[k * nch]
+        CK(cudaMemcpy2DAsync(ix_cptr_.p, sizeof(uint64_t), ix_off_.p, sizeof(uint64_t) * nch, sizeof(uint64_t), k_ + 1,
+                             cudaMemcpyDeviceToDevice, stream_));
+        uint64_t nnz_c = 0;
+        CK(cudaMemcpyAsync(&nnz_c, ix_off_.p + ncnt, 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        if (nnz_c >= (1ull << 31)) throw std::runtime_error("ncc+index: centroid supports too large for the index build");
+        grow(ix_keys_, 2 * nnz_c + 1);
+        idx_support_fill_kernel<<<g2, 128, 0, stream_>>>(ct_.p, ld_, d_, k_, rows, nch, ix_off_.p, ix_keys_.p);
+        ++launches_;
+        CK_LAUNCH();
+        tmp = 0;
+        CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, ix_keys_.p, ix_keys_.p + nnz_c, static_cast<int>(nnz_c),
+                                              static_cast<int>(k_), ix_cptr_.p, ix_cptr_.p + 1, stream_));
+        grow(ix_tmp_, tmp);
+        CK(cub::DeviceSegmentedSort::SortKeys(ix_tmp_.p, tmp, ix_keys_.p, ix_keys_.p + nnz_c, static_cast<int>(nnz_c),
+                                              static_cast<int>(k_), ix_cptr_.p, ix_cptr_.p + 1, stream_));
+        ++launches_;
+        const uint64_t* keys = ix_keys_.p + nnz_c;
+        // 2. windows per (λ, centroid)
+        ix_lam_.alloc(L);
+        CK(cudaMemcpyAsync(ix_lam_.p, lambdas_.data(), sizeof(double) * L, cudaMemcpyHostToDevice, stream_));
+        grow(ix_mval_, static_cast<size_t>(L) * nnz_c + 1);
+        ix_jlen_.alloc(static_cast<size_t>(L) * k_);
+        launch(idx_window_kernel, static_cast<unsigned>(ceil_div(static_cast<int64_t>(k_) * L * 32, 128)), 128, keys,
+               ix_cptr_.p, k_, ix_lam_.p, L, nnz_c, ix_mval_.p, ix_jlen_.p);
+        CK_LAUNCH();
+        CK(cudaEventRecord(ev_[7], stream_));
+        // 3. per-document rescan flags and λ selection
+        ix_rescan_.alloc(n_);
+        if (last_full_equiv_) {
+            launch(idx_rescan_formula_kernel, grid_for(n_, 256), 256, a_start_.p, sims_start_.p, sims_.p,
+                   unchanged_.p, n_, ix_rescan_.p);
+        } else {
+            CK(cudaMemsetAsync(ix_rescan_.p, 0, n_, stream_));
+            if (last_n_rescan_ > 0)
+                launch(idx_rescan_scatter_kernel, grid_for(static_cast<int64_t>(last_n_rescan_), 256), 256, rescan_.p,
+                       static_cast<int64_t>(last_n_rescan_), ix_rescan_.p);
+        }
+        ix_sel_.alloc(n_);
+        ix_list_.alloc(n_);
+        ix_ctr_.alloc(5);
+        CK(cudaMemsetAsync(ix_ctr_.p, 0, 5 * sizeof(unsigned long long), stream_));
+        IndexSelArgs sa{};
+        sa.indptr = indptr_.p;
+        sa.idx = idx_.p;
+        sa.val = val_.p;
+        sa.CT = ct_.p;
+        sa.ld_ct = ld_;
+        sa.n = n_;
+        sa.a_start = a_start_.p;
+        sa.sims_start = sims_start_.p;
+        sa.unchanged = unchanged_.p;
+        sa.rescan = ix_rescan_.p;
+        sa.lambdas = ix_lam_.p;
+        sa.n_lambdas = L;
+        sa.n_changed = n_chg_;
+        sa.n_unchanged = k_ - n_chg_;
+        sa.sel = ix_sel_.p;
+        sa.counters = ix_ctr_.p;
+        launch(idx_select_kernel, grid_for(n_ * 32, 256), 256, sa);
+        CK_LAUNCH();
+        // 4. queries, per cluster tile and λ
+        constexpr uint32_t KT = 1024;
+        auto qk = idx_query_kernel<KT>;
+        const int warps = 8;
+        const size_t smem = static_cast<size_t>(warps) * 2 * KT * sizeof(uint32_t);
+        CK(cudaFuncSetAttribute(qk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qk, warps * 32, smem));
+        ix_lcnt_.alloc(d_ + 1);
+        ix_lptr_.alloc(d_ + 1);
+        ix_fill_.alloc(d_);
+        // documents grouped by λ: one compact pass per λ into consecutive ranges
+        std::vector<int64_t> l_beg(L + 1, 0);
+        {
+            int64_t pos = 0;
+            for (uint32_t l = 0; l < L; ++l) {
+                CK(cudaMemsetAsync(ix_ctr_.p + 4, 0, 8, stream_));
+                launch(idx_compact_kernel, grid_for(n_, 256), 256, ix_sel_.p, n_, l, ix_list_.p + pos, ix_ctr_.p + 4);
+                unsigned long long m = 0;
+                CK(cudaMemcpyAsync(&m, ix_ctr_.p + 4, 8, cudaMemcpyDeviceToHost, stream_));
+                CK(cudaStreamSynchronize(stream_));
+                l_beg[l] = pos;
+                pos += static_cast<int64_t>(m);
+                l_beg[l + 1] = pos;
+            }
+        }
+        for (uint32_t c0 = 0; c0 < k_; c0 += KT) {
+            const uint32_t kt = std::min<uint32_t>(KT, k_ - c0);
+            bool built = false;
+            for (uint32_t l = 0; l < L; ++l) {
+                const int64_t nl = l_beg[l + 1] - l_beg[l];
+                if (nl == 0) continue;
+                if (!built) {
+                    build_postings(ct_.p, ld_, c0, kt);  // general postings of the tile
+                    built = true;
+                }
+                const uint32_t* jl = ix_jlen_.p + static_cast<size_t>(l) * k_;
+                const uint32_t* mv = ix_mval_.p + static_cast<size_t>(l) * nnz_c;
+                CK(cudaMemsetAsync(ix_lcnt_.p, 0, sizeof(uint32_t) * (d_ + 1), stream_));
+                launch(idx_lam_count_kernel, static_cast<unsigned>(ceil_div(static_cast<int64_t>(kt) * 32, 256)), 256,
+                       keys, ix_cptr_.p, jl, c0, kt, ix_lcnt_.p);
+                size_t t2 = 0;
+                CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, ix_lcnt_.p, ix_lptr_.p, static_cast<int>(d_ + 1),
+                                                 stream_));
+                grow(ix_tmp_, t2);
+                CK(cub::DeviceScan::ExclusiveSum(ix_tmp_.p, t2, ix_lcnt_.p, ix_lptr_.p, static_cast<int>(d_ + 1),
+                                                 stream_));
+                ++launches_;
+                uint32_t tot = 0;
+                CK(cudaMemcpyAsync(&tot, ix_lptr_.p + d_, 4, cudaMemcpyDeviceToHost, stream_));
+                CK(cudaStreamSynchronize(stream_));
+                grow(ix_lent_, static_cast<size_t>(tot) + 1);
+                CK(cudaMemsetAsync(ix_fill_.p, 0, sizeof(uint32_t) * d_, stream_));
+                launch(idx_lam_fill_kernel, static_cast<unsigned>(ceil_div(static_cast<int64_t>(kt) * 32, 256)), 256,
+                       keys, ix_cptr_.p, jl, mv, c0, kt, ix_lptr_.p, ix_fill_.p, ix_lent_.p);
+                IndexQueryArgs q{};
+                q.indptr = indptr_.p;
+                q.idx = idx_.p;
+                q.gptr = pptr_.p;
+                q.gpairs = pairs_.p;
+                q.lptr = ix_lptr_.p;
+                q.lent = ix_lent_.p;
+                q.c0 = c0;
+                q.kt = kt;
+                q.list = ix_list_.p + l_beg[l];
+                q.n_list = nl;
+                q.a_start = a_start_.p;
+                q.unchanged = unchanged_.p;
+                q.rescan = ix_rescan_.p;
+                q.counters = ix_ctr_.p;
+                const unsigned grid = static_cast<unsigned>(
+                    std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms_) * std::max(1, per_sm),
+                                                           ceil_div(nl, warps))));
+                qk<<<grid, warps * 32, smem, stream_>>>(q);
+                ++launches_;
+                CK_LAUNCH();
+            }
+        }
+        unsigned long long ctr[4] = {0, 0, 0, 0};
+        CK(cudaMemcpyAsync(ctr, ix_ctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        float build_ms = 0.f;
+        CK(cudaEventElapsedTime(&build_ms, ev_[6], ev_[7]));
+        st->index_active = 1;
+        st->index_build_seconds = build_ms * 1e-3;
+        st->index_queries = ctr[0];
+        st->candidates_total = ctr[2];
+        st->dot_products = st->dot_products - ctr[1] + ctr[3];
     }
 
     void full_assign(sskm_iteration_stats* st) {
@@ -498,6 +691,8 @@ public:
             }
         }
         CK(cudaEventRecord(ev_[5], stream_));
+        last_full_equiv_ = n_chg_ > 0 && full_equiv;
+        last_n_rescan_ = n_rescan;
         finish_assign(st);
         cache_trusted_ = true;
         // dot accounting of the reference (engine.cpp:253-306): every document
@@ -1041,6 +1236,27 @@ private:
 
     // Inverted-index screen, one cluster tile at a time: build the tile's
     // postings from the dense columns, then run the warp-per-document screen.
+    // Postings of the columns [c0, c0 + kt) of M into pptr_ / pairs_: per-term
+    // counts, exclusive scan, bank-interleaved fill. Returns the pair count.
+    uint32_t build_postings(const float* M, uint64_t ld, uint32_t c0, uint32_t kt) {
+        pcnt_.alloc(d_ + 1);
+        pptr_.alloc(d_ + 1);
+        CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
+        launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt, pcnt_.p);
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
+        scan_tmp_.alloc(tmp);
+        CK(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
+        ++launches_;
+        uint32_t total = 0;
+        CK(cudaMemcpyAsync(&total, pptr_.p + d_, 4, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        if (total > pairs_.n) pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
+        launch(postings_fill_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt, pptr_.p,
+               pairs_.p);
+        return total;
+    }
+
     void postings_screen(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
                          const uint32_t* order, int64_t n_work, int fuse) {
         sb_.alloc(n_);
@@ -1065,21 +1281,7 @@ private:
         p.r = resolve_args(order, n_work);
         for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
             const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
-            // postings of columns [c0, c0 + kt)
-            CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
-            launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt,
-                   pcnt_.p);
-            size_t tmp = 0;
-            CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
-            scan_tmp_.alloc(tmp);
-            CK(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
-            ++launches_;
-            uint32_t total = 0;
-            CK(cudaMemcpyAsync(&total, pptr_.p + d_, 4, cudaMemcpyDeviceToHost, stream_));
-            CK(cudaStreamSynchronize(stream_));
-            if (total > pairs_.n) pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
-            launch(postings_fill_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt,
-                   pptr_.p, pairs_.p);
+            const uint32_t total = build_postings(M, ld, c0, kt);
             p.pptr = pptr_.p;
             p.pairs = pairs_.p;
             if (c0 == 0) last_density_ = static_cast<double>(total) / (static_cast<double>(d_) * kt);
@@ -1325,6 +1527,16 @@ private:
     DevBuf<int64_t> indptr_;
     DevBuf<int32_t> idx_;
     DevBuf<float> val_;
+    // ncc+index accounting (index_account)
+    DevBuf<uint32_t> ix_cnt_, ix_mval_, ix_jlen_, ix_lcnt_, ix_lptr_, ix_fill_, ix_list_;
+    DevBuf<uint64_t> ix_off_, ix_cptr_, ix_keys_;
+    DevBuf<unsigned long long> ix_ctr_;
+    DevBuf<double> ix_lam_;
+    DevBuf<uint8_t> ix_sel_, ix_rescan_;
+    DevBuf<uint2> ix_lent_;
+    DevBuf<char> ix_tmp_;
+    bool last_full_equiv_ = false;
+    uint64_t last_n_rescan_ = 0;
     DevBuf<float> ct_, cc_;
     DevBuf<long long> S_;
     DevBuf<uint32_t> a_, a_sum_, a_start_, moved_, rescan_, rec_ids_, rec_pos_, chg_ids_;
@@ -1422,7 +1634,10 @@ void step(Engine& e, sskm_iteration_stats* st) {
     st->screen_launches = a.screen_launches;
     st->centroid_density = a.centroid_density;
     st->n_exact = a.n_exact;
-    st->index_active = 0;
+    st->index_active = a.index_active;
+    st->index_queries = a.index_queries;
+    st->candidates_total = a.candidates_total;
+    st->index_build_seconds = a.index_build_seconds;
     st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 }  // namespace

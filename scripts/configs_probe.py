@@ -16,7 +16,8 @@ for it in range(1, iters + 1):
     print(json.dumps(dict(iter=it, ms=round(eng.timer_elapsed(0, 1), 2), update_ms=round(st.update_ms, 2),
                           assign_ms=round(st.assign_ms, 2), screen_ms=round(st.screen_ms, 2), tiles=st.screen_launches,
                           n_changed=st.n_changed, density=round(st.centroid_density, 4), n_reassigned=st.n_reassigned, n_exact=st.n_exact,
-                          n_rescan=st.n_rescan, n_repaired=st.n_repaired, dots=st.dot_products)), flush=True)
+                          n_rescan=st.n_rescan, n_repaired=st.n_repaired, dots=st.dot_products,
+                          **({} if not st.index_active else dict(idx_build_ms=round(st.index_build_seconds * 1e3, 2), idx_queries=st.index_queries, idx_cands=st.candidates_total)))), flush=True)
 if os.environ.get("PROBE_PAIRS"):
     pairs = eng.postings_work()
     print(json.dumps(dict(postings_pairs=pairs, mean_dfc_per_entry=pairs / data.nnz,
