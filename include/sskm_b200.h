@@ -27,7 +27,9 @@ extern "C" {
 /* Mode, engine.hpp:13 (parse_mode, engine.cpp:21-27). */
 #define SSKM_MODE_BASELINE 0
 #define SSKM_MODE_NCC 1
-#define SSKM_MODE_NCC_INDEX 2 /* runs the exact NCC kernels; index_active stays 0 */
+#define SSKM_MODE_NCC_INDEX 2 /* assignment by the exact NCC kernels; when the reference would build its
+                                 Lemma-1 index (engine.cpp:384-386) the index is rebuilt on the GPU and
+                                 its queries replayed: index_* counters and dot_products are the reference's */
 
 /* StopReason, engine.hpp:59 */
 #define SSKM_STOP_NO_REASSIGNMENTS 0
@@ -39,7 +41,7 @@ extern "C" {
 typedef struct {
     uint32_t k;
     int32_t mode;
-    const double* lambdas; /* validated like the reference; the index is not built */
+    const double* lambdas; /* validated like the reference; thresholds of the ncc+index index */
     uint32_t n_lambdas;
     double conv_sq_dist;
     double ncc_epsilon;
