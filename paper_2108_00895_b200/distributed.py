@@ -306,17 +306,19 @@ class DistributedKMeans:
 
     def assign(self) -> IterationStats:
         st = self.s.assign()
-        tot = self.comm.all_reduce_i64(np.array([st.n_reassigned, st.n_rescan, st.n_exact, st.gpu_dot_products],
+        # every counter is a sum over documents (the reference's accounting is
+        # per document, engine.cpp:244-312), so the global value is the sum of
+        # the ranks' local ones — in every mode, the ncc+index replay included
+        tot = self.comm.all_reduce_i64(np.array([st.n_reassigned, st.n_rescan, st.n_exact, st.gpu_dot_products,
+                                                 st.dot_products, st.index_queries, st.candidates_total],
                                                 np.int64))
         objs = self.comm.all_gather_f64(st.objective)
         obj = 0.0
         for o in objs:  # rank order: deterministic for a given world size
             obj += o
-        n_unch = st.n_unchanged_centroids
-        full = self.iteration <= 1 or self.mode == "baseline"
-        dots = self.k * self.n_total if full else self.n_total * (self.k - n_unch) + int(tot[1]) * n_unch
         return replace(st, n_reassigned=int(tot[0]), n_rescan=int(tot[1]), n_exact=int(tot[2]),
-                       gpu_dot_products=int(tot[3]), objective=obj, dot_products=dots)
+                       gpu_dot_products=int(tot[3]), objective=obj, dot_products=int(tot[4]),
+                       index_queries=int(tot[5]), candidates_total=int(tot[6]))
 
     def step(self) -> IterationStats:
         u = self.update()

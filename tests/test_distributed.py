@@ -112,7 +112,8 @@ class NumpyShard:
         for s in self.sims:
             obj += s
         return IterationStats(n_reassigned=int(np.sum(self.a != a0)), objective=obj,
-                              n_unchanged_centroids=0, gpu_dot_products=self.k * self.m.n_docs)
+                              n_unchanged_centroids=0, gpu_dot_products=self.k * self.m.n_docs,
+                              dot_products=self.k * self.m.n_docs)
 
 
 def corpus_with_duplicate_seeds():

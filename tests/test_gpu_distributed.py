@@ -34,6 +34,16 @@ def corpus_and_seeds():
     return data, seeds
 
 
+def _cfg(mode):
+    # ncc+index: a low activation threshold so the replayed index is active
+    return dict(mode=mode, conv_sq_dist=1e-300, index_activation_threshold=2 if mode == "ncc+index" else 100)
+
+
+def _stats(st):
+    return (st.n_reassigned, st.n_repaired, st.dot_products, st.index_queries, st.candidates_total,
+            bool(st.index_active), st.max_sq_drift, st.objective)
+
+
 def _worker(rank, world, port, mode, q):
     import torch.distributed as dist
 
@@ -43,7 +53,7 @@ def _worker(rank, world, port, mode, q):
     try:
         data, seeds = corpus_and_seeds()
         shard, off = D.shard_corpus(data, rank, world)
-        gs = D.GPUShard(shard, off, data.n_docs, len(seeds), device=0, mode=mode, conv_sq_dist=1e-300)
+        gs = D.GPUShard(shard, off, data.n_docs, len(seeds), device=0, **_cfg(mode))
         comm = D.Comm(rank, world, torch.device("cpu"))
         km = D.DistributedKMeans(gs, comm, data.n_docs, len(seeds), mode=mode, conv_sq_dist=1e-300)
         km.init_from_seeds(seeds)
@@ -53,8 +63,7 @@ def _worker(rank, world, port, mode, q):
             a, s, _ = gs.get_state()
             ag = torch.cat(comm.all_gather_var(torch.as_tensor(a.astype(np.int64)))).numpy()
             sg = torch.cat(comm.all_gather_var(torch.as_tensor(s))).numpy()
-            trace.append((ag, sg, gs.get_centroids(), (st.n_reassigned, st.n_repaired, st.dot_products,
-                                                       st.max_sq_drift, st.objective)))
+            trace.append((ag, sg, gs.get_centroids(), _stats(st)))
         if rank == 0:
             q.put(trace)
     finally:
@@ -79,19 +88,18 @@ def run_sharded(world, mode):
     return out
 
 
-@pytest.mark.parametrize("mode", ["baseline", "ncc"])
+@pytest.mark.parametrize("mode", ["baseline", "ncc", "ncc+index"])
 def test_two_shards_equal_single_gpu(mode):
     data, seeds = corpus_and_seeds()
     eng = P.Engine(0)
     eng.upload(data)
-    eng.configure(len(seeds), mode=mode, conv_sq_dist=1e-300)
+    eng.configure(len(seeds), **_cfg(mode))
     eng.init_from_seeds(seeds)
     single = []
     for _ in range(ITERS):
         st = eng.step()
         a, s, _ = eng.get_state()
-        single.append((a.astype(np.int64), s, eng.get_centroids(),
-                       (st.n_reassigned, st.n_repaired, st.dot_products, st.max_sq_drift, st.objective)))
+        single.append((a.astype(np.int64), s, eng.get_centroids(), _stats(st)))
     eng.close()
     two = run_sharded(2, mode)
     assert single[0][3][1] == 1  # repair happened (duplicated seed on the other shard)
@@ -99,5 +107,7 @@ def test_two_shards_equal_single_gpu(mode):
         assert np.array_equal(a1, a2), t
         assert np.array_equal(s1, s2), t
         assert np.array_equal(c1, c2), t
-        assert x1[:4] == x2[:4], (t, x1, x2)
-        assert x2[4] == pytest.approx(x1[4], rel=1e-12)
+        assert x1[:7] == x2[:7], (t, x1, x2)
+        assert x2[7] == pytest.approx(x1[7], rel=1e-12)
+    if mode == "ncc+index":
+        assert any(x[5] for _, _, _, x in single)
