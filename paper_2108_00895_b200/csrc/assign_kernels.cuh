@@ -729,15 +729,19 @@ __global__ void postings_work_kernel(const int32_t* __restrict__ idx, int64_t nn
 // accumulator banks. Lane l scans columns j = l (mod 32), i.e. exactly bank l
 // (tiles start at multiples of 32). The order inside one list never changes a
 // result: every cluster occurs once per list.
+// Entries kept in a postings build: nonzero and |v| >= thr (thr = 0: every
+// nonzero; thr > 0: the high entries of the bound screen).
+__device__ __forceinline__ bool post_keep(float v, float thr) { return v != 0.f && fabsf(v) >= thr; }
+
 __global__ void postings_count_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d, uint32_t c0,
-                                      uint32_t kt, uint32_t* __restrict__ cnt) {
+                                      uint32_t kt, uint32_t* __restrict__ cnt, float thr) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
     for (uint64_t t = gw; t < d; t += nw) {
         const float* row = M + t * ld + c0;
         int c = 0;
-        for (uint32_t j = lane; j < kt; j += kWarp) c += row[j] != 0.f;
+        for (uint32_t j = lane; j < kt; j += kWarp) c += post_keep(row[j], thr);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, off);
         if (lane == 0) cnt[t] = c;
@@ -746,7 +750,7 @@ __global__ void postings_count_kernel(const float* __restrict__ M, uint64_t ld, 
 
 __global__ void __launch_bounds__(256) postings_fill_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
                                                             uint32_t c0, uint32_t kt, const uint32_t* __restrict__ pptr,
-                                                            uint2* __restrict__ pairs) {
+                                                            uint2* __restrict__ pairs, float thr) {
     constexpr int kMaxRank = 64;  // kt <= 2048 clusters per tile
     __shared__ uint32_t s_mask[8][kMaxRank], s_base[8][kMaxRank];
     const int lane = threadIdx.x & (kWarp - 1);
@@ -758,7 +762,7 @@ __global__ void __launch_bounds__(256) postings_fill_kernel(const float* __restr
     for (uint64_t t = gw; t < d; t += nw) {
         const float* row = M + t * ld + c0;
         uint32_t cnt = 0;
-        for (uint32_t j = lane; j < kt; j += kWarp) cnt += row[j] != 0.f;
+        for (uint32_t j = lane; j < kt; j += kWarp) cnt += post_keep(row[j], thr);
         uint32_t run = 0;
         for (int r = 0; r < ranks; ++r) {
             const unsigned m = __ballot_sync(0xFFFFFFFFu, cnt > static_cast<uint32_t>(r));
@@ -773,7 +777,7 @@ __global__ void __launch_bounds__(256) postings_fill_kernel(const float* __restr
         uint32_t r = 0;
         for (uint32_t j = lane; j < kt; j += kWarp) {
             const float v = row[j];
-            if (v != 0.f) {
+            if (post_keep(v, thr)) {
                 pairs[base + s_base[wib][r] + __popc(s_mask[wib][r] & lt)] = make_uint2(j, __float_as_uint(v));
                 ++r;
             }

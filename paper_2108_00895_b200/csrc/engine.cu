@@ -8,6 +8,7 @@
 //   assign  = assign (:218-322) + objective Σ sims (:403-405)
 //   run     = stop on no reassignment (:409-412) or drift < conv_sq_dist after iteration 1 (:413-416)
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <climits>
 #include <cstdlib>
@@ -24,6 +25,7 @@
 
 #include "../../include/sskm_b200.h"
 #include "assign_kernels.cuh"
+#include "bound_kernels.cuh"
 #include "common.cuh"
 #include "index_kernels.cuh"
 #include "update_kernels.cuh"
@@ -85,6 +87,12 @@ public:
         if (const char* e = std::getenv("SSKM_ORDER")) order_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_DEBUG")) debug_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_THETA")) {
+            theta_ = static_cast<float>(std::atof(e));
+            theta_adapt_ = false;
+        }
         if (const char* e = std::getenv("SSKM_POST_KT")) post_kt_max_ = static_cast<uint32_t>(std::atoi(e));
         if (const char* e = std::getenv("SSKM_POST_WARPS")) post_warps_ = std::max(1, std::min(8, std::atoi(e)));
         if (const char* e = std::getenv("SSKM_DENSE_ABOVE")) dense_above_ = std::atof(e);
@@ -173,6 +181,8 @@ public:
         nonneg_ = (hs_->bad & 16u) == 0;
         xnorm2_.alloc(n);
         launch(doc_norm2_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p);
+        xnorm1_.alloc(n);
+        launch(doc_norm1_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm1_.p);
         CK_LAUNCH();
         // fixed-point scale: N_total · 2^K <= 2^62 with |x| <= 1
         int lg = 0;
@@ -1207,8 +1217,168 @@ private:
     }
 
     // Returns true when the screen also certified (fused resolve).
+    // ------------------------------------------------------- bound screen --
+    // Exact assignment from the high centroid entries (bound_kernels.cuh).
+    void bound_assign(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* order,
+                      int64_t n_work, int init) {
+        btake_.alloc(n_);
+        bwork_.alloc(n_);
+        bctr_.alloc(4);
+        CK(cudaMemsetAsync(bctr_.p, 0, 4 * sizeof(unsigned long long), stream_));
+        const float thr = theta_;
+        BoundInitArgs ia{};
+        ia.indptr = indptr_.p;
+        ia.idx = idx_.p;
+        ia.val = val_.p;
+        ia.CT = ct_.p;
+        ia.ld_ct = ld_;
+        ia.order = order;
+        ia.n_work = n_work;
+        ia.xnorm2 = xnorm2_.p;
+        ia.xnorm1 = xnorm1_.p;
+        ia.theta = static_cast<double>(thr);
+        ia.cmax = cmax_;
+        ia.k = k_;
+        ia.a = a_.p;
+        ia.sims = sims_.p;
+        ia.unchanged = unchanged_.p;
+        ia.a_start = a_start_.p;
+        ia.sims_start = sims_start_.p;
+        ia.take = btake_.p;
+        ia.exact_list = exact_.p;
+        ia.n_exact = &scal_.p->n_exact;
+        if (init == kInitFull)
+            launch(bound_init_kernel<kInitFull>, grid_for(n_work * 32, 256), 256, ia);
+        else if (init == kInitNcc)
+            launch(bound_init_kernel<kInitNcc>, grid_for(n_work * 32, 256), 256, ia);
+        else
+            launch(bound_init_kernel<kInitRescan>, grid_for(n_work * 32, 256), 256, ia);
+        CK_LAUNCH();
+        // documents taken by the bound screen, in work-list (cluster) order
+        size_t tmp = 0;
+        cub::CountingInputIterator<uint32_t> iota(0);
+        if (order) {
+            CK(cub::DeviceSelect::Flagged(nullptr, tmp, order, btake_.p, bwork_.p, bctr_.p + 3,
+                                          static_cast<int>(n_work), stream_));
+            grow_tmp(tmp);
+            CK(cub::DeviceSelect::Flagged(bsel_tmp_.p, tmp, order, btake_.p, bwork_.p, bctr_.p + 3,
+                                          static_cast<int>(n_work), stream_));
+        } else {
+            CK(cub::DeviceSelect::Flagged(nullptr, tmp, iota, btake_.p, bwork_.p, bctr_.p + 3,
+                                          static_cast<int>(n_work), stream_));
+            grow_tmp(tmp);
+            CK(cub::DeviceSelect::Flagged(bsel_tmp_.p, tmp, iota, btake_.p, bwork_.p, bctr_.p + 3,
+                                          static_cast<int>(n_work), stream_));
+        }
+        ++launches_;
+        unsigned long long n_list = 0;
+        CK(cudaMemcpyAsync(&n_list, bctr_.p + 3, 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        if (n_list > 0) {
+            const uint32_t KT = ncols <= 1024 ? 1024 : 2048;
+            BoundArgs p{};
+            p.indptr = indptr_.p;
+            p.idx = idx_.p;
+            p.val = val_.p;
+            p.col_ids = col_ids;
+            p.list = bwork_.p;
+            p.n_list = static_cast<int64_t>(n_list);
+            p.CT = ct_.p;
+            p.ld_ct = ld_;
+            p.xnorm2 = xnorm2_.p;
+            p.xnorm1 = xnorm1_.p;
+            p.theta = static_cast<double>(thr);
+            p.cmax = cmax_;
+            p.a = a_.p;
+            p.sims = sims_.p;
+            p.n_cand = bctr_.p + 0;
+            p.n_pairs = bctr_.p + 1;
+            p.k = k_;
+            if (col_ids) {  // cluster -> column of M
+                bcol_of_.alloc(k_);
+                launch(fill_u32_kernel, grid_for(k_, 256), 256, bcol_of_.p, static_cast<int64_t>(k_), kNone);
+                launch(scatter_pos_kernel, grid_for(ncols, 256), 256, col_ids, ncols, bcol_of_.p);
+                p.col_of = bcol_of_.p;
+            }
+            for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
+                const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
+                build_postings(M, ld, c0, kt, thr);
+                p.pptr = pptr_.p;
+                p.pairs = pairs_.p;
+                p.c0 = c0;
+                p.kt = kt;
+                CK(cudaEventRecord(ev_[6], stream_));
+                if (KT == 1024)
+                    bound_launch<1024>(p);
+                else
+                    bound_launch<2048>(p);
+                CK(cudaEventRecord(ev_[7], stream_));
+                CK(cudaEventSynchronize(ev_[7]));
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
+                screen_ms_ += ms;
+                screen_launches_ += 1;
+            }
+            if (init == kInitNcc)
+                launch(bound_ncc_rescan_kernel, grid_for(static_cast<int64_t>(n_list), 256), 256, bwork_.p,
+                       static_cast<int64_t>(n_list), a_start_.p, sims_start_.p, sims_.p, unchanged_.p, rescan_.p,
+                       &scal_.p->n_rescan);
+        }
+        // θ for the next assign: keep the exact-scan share small and the
+        // candidate dots near one per document (θ never changes a result)
+        unsigned long long ctr[2] = {0, 0};
+        uint64_t n_fb = 0;
+        CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(&n_fb, &scal_.p->n_exact, 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        last_bound_cand_ = ctr[0];
+        last_bound_pairs_ = ctr[1];
+        last_bound_list_ = n_list;
+        if (debug_)
+            std::fprintf(stderr, "[sskm] bound init=%d theta=%.5g work=%lld list=%llu exact=%llu cand=%llu pairs=%llu\n",
+                         init, static_cast<double>(thr), static_cast<long long>(n_work),
+                         static_cast<unsigned long long>(n_list), static_cast<unsigned long long>(n_fb),
+                         static_cast<unsigned long long>(ctr[0]), static_cast<unsigned long long>(ctr[1]));
+        if (theta_adapt_ && n_work > 0) {
+            const double fb = static_cast<double>(n_fb) / static_cast<double>(n_work);
+            const double cpd = n_list ? static_cast<double>(ctr[0]) / static_cast<double>(n_list) : 0.0;
+            if (fb > 2e-3 || cpd > 2.0)
+                theta_ *= 0.7f;
+            else if (cpd < 0.3)
+                theta_ *= 1.25f;
+            theta_ = std::min(0.25f, std::max(1e-5f, theta_));
+        }
+    }
+
+    template <int KT>
+    void bound_launch(const BoundArgs& p) {
+        auto k = bound_screen_kernel<KT>;
+        const size_t per_warp = BoundSmem<KT>::per_warp;
+        const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (100u << 10) / per_warp)));
+        const size_t smem = static_cast<size_t>(warps) * per_warp;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem));
+        per_sm = std::max(1, per_sm);
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(p.n_list, warps))));
+        k<<<grid, warps * 32, smem, stream_>>>(p);
+        ++launches_;
+        CK_LAUNCH();
+    }
+
+    void grow_tmp(size_t n) {
+        if (n > bsel_tmp_.n) bsel_tmp_.alloc(n + n / 4 + 256);
+    }
+
     bool screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
                     const uint32_t* order, int64_t n_work, int init) {
+        // the bound screen needs a real assignment to start from: not the
+        // seed assignment (iteration 0), whose state is all cluster 0
+        if (bound_enabled_ && iteration_ >= 1) {
+            bound_assign(M, ld, ncols, col_ids, order, n_work, init);
+            return true;  // candidates resolved exactly in the kernel; the exact list holds the rest
+        }
         // postings move 8 B per nonzero centroid weight at ~4 TB/s, the dense
         // screen 4 B per weight mostly from L2 at ~12 TB/s: above ~15% density
         // (long documents, few clusters: c3) the dense screen wins (measured)
@@ -1217,7 +1387,7 @@ private:
             const uint32_t kt = std::min<uint32_t>(ncols, 2048);
             CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
             launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, 0u, kt,
-                   pcnt_.p);
+                   pcnt_.p, 0.f);
             size_t tmp = scan_tmp_.n;
             CK(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
             uint32_t total = 0;
@@ -1238,11 +1408,12 @@ private:
     // postings from the dense columns, then run the warp-per-document screen.
     // Postings of the columns [c0, c0 + kt) of M into pptr_ / pairs_: per-term
     // counts, exclusive scan, bank-interleaved fill. Returns the pair count.
-    uint32_t build_postings(const float* M, uint64_t ld, uint32_t c0, uint32_t kt) {
+    uint32_t build_postings(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr = 0.f) {
         pcnt_.alloc(d_ + 1);
         pptr_.alloc(d_ + 1);
         CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
-        launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt, pcnt_.p);
+        launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt, pcnt_.p,
+               thr);
         size_t tmp = 0;
         CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, pcnt_.p, pptr_.p, static_cast<int>(d_ + 1), stream_));
         scan_tmp_.alloc(tmp);
@@ -1253,7 +1424,7 @@ private:
         CK(cudaStreamSynchronize(stream_));
         if (total > pairs_.n) pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
         launch(postings_fill_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, M, ld, d_, c0, kt, pptr_.p,
-               pairs_.p);
+               pairs_.p, thr);
         return total;
     }
 
@@ -1321,7 +1492,7 @@ public:
             const uint32_t kt = std::min<uint32_t>(KT, k_ - c0);
             CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
             launch(postings_count_kernel, grid_for(static_cast<int64_t>(d_) * 32, 256), 256, ct_.p, (uint64_t)ld_, d_,
-                   c0, kt, pcnt_.p);
+                   c0, kt, pcnt_.p, 0.f);
             CK(cudaMemsetAsync(&scal_.p->n_moved, 0, 8, stream_));
             launch(postings_work_kernel, grid_for(nnz_, 256), 256, idx_.p, nnz_, pcnt_.p, &scal_.p->n_moved);
             CK_LAUNCH();
@@ -1527,6 +1698,11 @@ private:
     DevBuf<int64_t> indptr_;
     DevBuf<int32_t> idx_;
     DevBuf<float> val_;
+    DevBuf<double> xnorm1_;
+    DevBuf<uint8_t> btake_;
+    DevBuf<uint32_t> bwork_, bcol_of_;
+    DevBuf<unsigned long long> bctr_;
+    DevBuf<unsigned char> bsel_tmp_;
     // ncc+index accounting (index_account)
     DevBuf<uint32_t> ix_cnt_, ix_mval_, ix_jlen_, ix_lcnt_, ix_lptr_, ix_fill_, ix_list_;
     DevBuf<uint64_t> ix_off_, ix_cptr_, ix_keys_;
@@ -1552,7 +1728,12 @@ private:
     uint32_t post_kt_max_ = 1024;
     int post_warps_ = 8;
     bool cache_trusted_ = false;
-    bool fuse_resolve_ = false;  // measured: fusing costs the screen occupancy (c1 13.3 -> 18.0 ms)
+    bool fuse_resolve_ = false;
+    bool bound_enabled_ = true;   // bound screen (SSKM_BOUND=0: the full postings / dense screens)
+    bool theta_adapt_ = true;
+    bool debug_ = false;  // SSKM_DEBUG=1: per-assign screen counters on stderr
+    float theta_ = 0.004f;        // high/low split of the centroid weights (SSKM_THETA)
+    uint64_t last_bound_cand_ = 0, last_bound_pairs_ = 0, last_bound_list_ = 0;  // measured: fusing costs the screen occupancy (c1 13.3 -> 18.0 ms)
     bool nonneg_ = true;
     double last_density_ = 0.0;
     double dense_above_ = 0.15;
