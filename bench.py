@@ -198,12 +198,17 @@ def algorithmic_assign_bytes(data, k):
     return 4 * nnz * k + 8 * nnz + 8 * (n + 1) + 24 * n
 
 
-def postings_assign_bytes(data, pairs):
-    """Bytes the postings screen must move per full-scan assign:
-    8 B per (cluster, value) pair + idx/val (8 B) and the two posting offsets
-    (8 B) per document nonzero + indptr + 24 B/doc of running top-2 state."""
-    n, nnz = data.n_docs, data.nnz
-    return 8 * pairs + 16 * nnz + 8 * (n + 1) + 24 * n
+def bound_screen_bytes(stats):
+    """Algorithmic bytes the bound screen moves per assign, from
+    the kernel's own counters: 8 B per high (cluster, value) pair, 16 B per
+    document nonzero (idx, val and the two posting offsets of its term), 36 B per
+    document visit (indptr pair, work-list id, running (arg, best) read and
+    written) and 4 B per centroid value gathered by a candidate's exact dot."""
+    m = lambda f: statistics.mean(getattr(s, f) for s in stats)
+    pairs, dnnz, visits, cnnz = m("bound_pairs"), m("bound_doc_nnz"), m("bound_visits"), m("bound_cand_nnz")
+    b = 8 * pairs + 16 * dnnz + 36 * visits + 4 * cnnz
+    return {"bytes": b, "high_pairs": pairs, "doc_nnz": dnnz, "visits": visits, "candidates": m("bound_candidates"),
+            "candidate_nnz": cnnz, "theta": m("bound_theta")}
 
 
 def run_ours(args):
@@ -242,12 +247,12 @@ def run_ours(args):
     performed = sum(s.gpu_dot_products for s in stats) / (total_ms / 1e3)
     kern_ms = [s.assign_kernel_ms for s in stats]
     peak, peak_src = measured_peak_gbs()
-    # dominant kernel: the postings screen (full-scan iterations: all k centroids)
-    pairs = eng.postings_work()
+    # dominant kernel: the bound screen (bound_screen_kernel, one launch per cluster tile)
     screen_ms = statistics.mean(s.screen_ms for s in stats)
     launches_per_assign = statistics.mean(s.screen_launches for s in stats)
-    bytes_post = postings_assign_bytes(data, pairs)
-    achieved = bytes_post / (screen_ms / 1e3) / 1e9
+    bb = bound_screen_bytes(stats)
+    achieved = bb["bytes"] / (screen_ms / 1e3) / 1e9
+    pairs_full = eng.postings_work()
     bytes_dense = algorithmic_assign_bytes(data, k)
     traffic, ncu = ncu_traffic()
     clocks = clk.summary()
@@ -264,14 +269,15 @@ def run_ours(args):
                      "screen": screen_ms},
         "uncertified_docs_per_iter": statistics.mean(s.n_exact for s in stats),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "postings_screen_kernel",
-                     "bytes_per_assign": bytes_post, "screen_ms_per_assign": screen_ms,
+                     "traffic": traffic, "kernel": "bound_screen_kernel",
+                     "bytes_per_assign": bb["bytes"], "bytes_breakdown": bb, "screen_ms_per_assign": screen_ms,
                      "launches_per_assign": launches_per_assign, "peak_source": peak_src,
-                     "postings_pairs_per_assign": pairs,
+                     "full_postings_pairs_per_assign": pairs_full,
                      "dense_equivalent": {"bytes": bytes_dense, "gbs": bytes_dense / (screen_ms / 1e3) / 1e9,
                                           "note": "SURVEY 8d B_assign (4·Σ nnz_i·k): what a dense Ct scan would move"},
-                     "note": "algorithmic bytes of the postings screen = 8·pairs + 16·nnz + 8·(N+1) + 24·N over "
-                             "the screen kernel's CUDA-event time; traffic = ncu dram bytes per launch"},
+                     "note": "algorithmic bytes of the bound screen = 8·high pairs + 16·doc nnz read + 36·doc visits "
+                             "+ 4·candidate-dot nnz (DESIGN.md §3.1), over the kernel's CUDA-event time; "
+                             "traffic = ncu dram bytes per launch"},
         "gpu_launches": launches,
         "clocks": clocks,
     }

@@ -83,6 +83,15 @@ typedef struct {
     uint32_t screen_launches; /* postings-screen launches in this assign (one per cluster tile) */
     uint32_t reserved0;
     double centroid_density;  /* nonzero fraction of the centroid tile last indexed (screen choice) */
+    /* bound screen (the default screen after the seed assignment) */
+    uint64_t bound_docs;       /* documents the bound screen resolved (summed over its passes) */
+    uint64_t bound_pairs;      /* high (cluster, value) pairs accumulated */
+    uint64_t bound_candidates; /* exact fp64 candidate dots */
+    uint64_t bound_doc_nnz;    /* document nonzeros read by the bound-screen launches (all tiles) */
+    uint64_t bound_cand_nnz;   /* document nonzeros of the candidate dots (= centroid values gathered) */
+    double bound_theta;        /* high/low split of the centroid weights used by the last pass */
+    uint64_t bound_visits;     /* documents visited by the bound-screen launches (all tiles) */
+    uint64_t bound_own_dots;   /* exact own-cluster dots computed inside the screen (the rest were cached) */
 } sskm_iteration_stats;
 
 typedef struct sskm_ctx sskm_ctx;

@@ -60,6 +60,14 @@ class sskm_iteration_stats(C.Structure):
         ("screen_launches", C.c_uint32),
         ("reserved0", C.c_uint32),
         ("centroid_density", C.c_double),
+        ("bound_docs", C.c_uint64),
+        ("bound_pairs", C.c_uint64),
+        ("bound_candidates", C.c_uint64),
+        ("bound_doc_nnz", C.c_uint64),
+        ("bound_cand_nnz", C.c_uint64),
+        ("bound_theta", C.c_double),
+        ("bound_visits", C.c_uint64),
+        ("bound_own_dots", C.c_uint64),
     ]
 
 

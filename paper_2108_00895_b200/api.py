@@ -119,6 +119,14 @@ class IterationStats:
     screen_launches: int = 0
     reserved0: int = 0
     centroid_density: float = 0.0
+    bound_docs: int = 0
+    bound_pairs: int = 0
+    bound_candidates: int = 0
+    bound_doc_nnz: int = 0
+    bound_cand_nnz: int = 0
+    bound_theta: float = 0.0
+    bound_visits: int = 0
+    bound_own_dots: int = 0
 
     @classmethod
     def from_c(cls, s: sskm_iteration_stats) -> "IterationStats":

@@ -2,293 +2,492 @@
 //
 // Split every centroid weight at a threshold θ. For a document x and cluster j,
 //   s_j = Σ_{t: |c_tj| ≥ θ} x_t c_tj  +  Σ_{t: 0 < |c_tj| < θ} x_t c_tj,
-// and the second sum is bounded by θ·‖x‖₁. So with acc_j the fp32 sum over
-// the high entries (postings built with |v| ≥ θ, a ~1-2% slice of all pairs on
-// the TF-IDF corpora: frequent terms carry small centroid weights),
-//   s_j ≤ UB_j = acc_j + δ + θ·‖x‖₁,  δ = (γ32(n+32) + γ64(n))·‖x‖₂·max‖c‖ + n·2^-126
-// bounds the reference's fp64 dot (sparse_vector.cpp:72-101) from above.
+// and the second sum is bounded by θ·‖x‖₁. The first sum is accumulated over
+// the "high postings" of the cluster tile (term → (cluster, value) with
+// |value| ≥ θ: a 1-2% slice of all centroid nonzeros on the TF-IDF corpora,
+// frequent terms carry small centroid weights) as an exact integer sum of
+// fixed-point products q_t = rn(fl32(x_t·c_tj)·2^30). Against the reference's
+// fp64 dot (sparse_vector.cpp:72-101):
+//   s_j ≤ UB_j = acc_j·2^-30 + θ·‖x‖₁ + (γ32(n+32) + γ64(n))·‖x‖₂·max‖c‖ + n·2^-30 + n·2^-126
+// (fp32 product rounding ≤ u32·Σ|x_t c_t| ≤ u32·‖x‖₂‖c‖, fixed-point rounding
+// ≤ 2^-31 per product, the reference's own fp64 rounding ≤ γ64·‖x‖₂‖c‖).
+// Integer addition is associative, so acc_j — and hence which clusters become
+// candidates — is independent of the order the lanes add in.
 //
 // Each document starts from an exact fp64 baseline (best, arg): its current
-// cluster (full scan), the cached or refreshed own similarity (NCC pass A,
-// engine.cpp:268-273) or the pass-A result (rescan, :303-305). A touched
-// cluster with UB_j ≥ best gets an exact fp64 dot (doc_col_dot_sm, bit-equal
-// to the reference) and the tie rule s > best || (s == best && j < arg)
-// (:259); an untouched cluster is bounded by θ·‖x‖₁ + γ64 alone, so documents
-// whose baseline does not beat that go to the exact scan instead. Every
-// cluster that could win or tie is evaluated exactly: the result is the
-// reference's argmax, independent of θ (θ only moves work between the
-// screen, the candidate dots and the exact scan).
+// cluster (full scan; the cached similarity when that column is bit-identical
+// to the one the cache was computed against), the cached or refreshed own
+// similarity (NCC pass A, engine.cpp:268-273) or the pass-A result (rescan,
+// :303-305). The own dot is computed inside the screen, its gathers issued with
+// the chunk's posting loads. A touched cluster with UB_j ≥ best gets an exact
+// fp64 dot (doc_col_dot_sm, bit-equal to the reference) and the tie rule
+// s > best || (s == best && j < arg) (:259); an untouched cluster is bounded by
+// θ·‖x‖₁ + γ64 alone, so documents whose baseline does not beat that go to the
+// exact scan instead. Every cluster that could win or tie is evaluated exactly:
+// the result is the reference's argmax, independent of θ (θ only moves work
+// between the screen, the candidate dots and the exact scan).
 #pragma once
 
 #include "assign_kernels.cuh"
 
 namespace sskm_b200 {
 
-struct BoundInitArgs {
-    const int64_t* indptr;
-    const int32_t* idx;
-    const float* val;
-    const float* CT;
-    uint64_t ld_ct;
-    const uint32_t* order;     // work item -> document (nullptr = identity)
-    int64_t n_work;
-    const double* xnorm2;
-    const double* xnorm1;
-    double theta, cmax;
-    uint32_t k;
-    uint32_t* a;               // in/out: running exact argmax
-    double* sims;              // in/out: running exact max
-    const uint8_t* unchanged;
-    const uint32_t* a_start;
-    const double* sims_start;
-    uint8_t* take;             // per work item: 1 = bound screen, 0 = exact scan
-    uint32_t* exact_list;      // documents for the exact scan
-    unsigned long long* n_exact;
-};
+#ifndef SSKM_BOUND_MINB
+#define SSKM_BOUND_MINB 4  // resident 256-thread blocks per SM the register budget is cut for
+#endif
 
-// θ·‖x‖₁ plus the fp64 rounding of the reference's dot: no cluster without a
-// high entry shared with x can exceed this.
-__device__ __forceinline__ double low_bound(double theta, double x1, double q, double n, double cmax) {
-    const double u64 = 0x1p-53;
-    const double g64 = n * u64 / (1.0 - n * u64);
-    return theta * x1 * (1.0 + 1e-12) + g64 * sqrt(q) * cmax * (1.0 + 1e-12) + n * 0x1p-126;
-}
-
-template <int INIT>
-__global__ void __launch_bounds__(256) bound_init_kernel(BoundInitArgs p) {
-    __shared__ __align__(16) double fold[256];
-    double* wsm = fold + (threadIdx.x & ~(kWarp - 1));
-    const int lane = threadIdx.x & (kWarp - 1);
-    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
-    for (uint64_t w = gw; w < static_cast<uint64_t>(p.n_work); w += nw) {
-        const int64_t i = p.order ? static_cast<int64_t>(p.order[w]) : static_cast<int64_t>(w);
-        const int64_t beg = p.indptr[i], end = p.indptr[i + 1];
-        double best;
-        uint32_t arg;
-        if constexpr (INIT == kInitFull) {
-            arg = p.a[i];
-            best = arg < p.k ? doc_col_dot_sm(p.idx, p.val, beg, end, p.CT, p.ld_ct, arg, lane, wsm) : -2.0;
-        } else if constexpr (INIT == kInitNcc) {
-            arg = p.a_start[i];
-            best = p.unchanged[arg] == 0 ? doc_col_dot_sm(p.idx, p.val, beg, end, p.CT, p.ld_ct, arg, lane, wsm)
-                                         : p.sims_start[i];
-        } else {
-            arg = p.a[i];
-            best = p.sims[i];
-        }
-        const double lb = low_bound(p.theta, p.xnorm1[i], p.xnorm2[i], static_cast<double>(end - beg), p.cmax);
-        const bool take = best > lb && (INIT != kInitFull || arg < p.k);
-        if (lane == 0) {
-            p.take[w] = take ? 1 : 0;
-            if (take) {
-                p.a[i] = arg;
-                p.sims[i] = best;
-            } else {
-                const unsigned long long pos = atomicAdd(p.n_exact, 1ull);
-                p.exact_list[pos] = static_cast<uint32_t>(i);
-            }
-        }
-    }
-}
+constexpr float kFixScale = 0x1p30f;    // fixed-point products: q = rn(p · 2^30)
+constexpr double kFixUnit = 0x1p-30;
 
 struct BoundArgs {
     const int64_t* indptr;
     const int32_t* idx;
     const float* val;
-    const uint32_t* pptr;      // high postings of the tile
-    const uint2* pairs;
+    const uint2* hptr;         // high postings of the tile: (first pair, count) per term
+    const uint2* pairs;        // (column in tile, value bits)
     uint32_t c0, kt;
     const uint32_t* col_ids;   // column -> cluster id (nullptr = identity)
     const uint32_t* col_of;    // cluster id -> column (kNone = absent); with col_ids
-    const uint32_t* list;      // documents taken by the bound screen
-    int64_t n_list;
-    const float* CT;
+    const uint32_t* order;     // work item -> document (nullptr = identity)
+    int64_t n_work;
+    const float* CT;           // full Cᵀ: own dots and candidate dots
     uint64_t ld_ct;
-    const double* xnorm2;
-    const double* xnorm1;
+    const float2* xb;          // per document (‖x‖₁, ‖x‖₂), rounded up
     double theta, cmax;
     uint32_t k;
-    uint32_t* a;
-    double* sims;
-    unsigned long long* n_cand;  // exact candidate dots
-    unsigned long long* n_pairs;  // high pairs accumulated (θ adaptation)
+    int first;                 // first tile: establish the baseline and decide take
+    uint32_t* a;               // in/out: running exact argmax
+    double* sims;              // in/out: running exact max
+    const uint8_t* unchanged;  // NCC: cached own similarity valid
+    const uint8_t* same;       // full scan: column bit-identical since the cache (nullptr = no cache)
+    const uint32_t* a_start;
+    const double* sims_start;
+    uint8_t* take;             // per work item: 1 = bound screen, 0 = exact scan
+    uint32_t* exact_list;      // documents for the exact scan
+    unsigned long long* n_exact;
+    unsigned long long* n_cand;      // exact candidate dots
+    unsigned long long* n_pairs;     // high pairs accumulated (θ adaptation)
+    unsigned long long* n_doc_nnz;   // document nonzeros read (roofline bytes)
+    unsigned long long* n_visits;    // documents visited, summed over tiles (roofline bytes)
+    unsigned long long* n_cand_nnz;  // nonzeros of the candidate dots (centroid values gathered)
+    unsigned long long* n_own;       // own dots computed in the screen
 };
 
-using PairT = uint2;
-__device__ __forceinline__ PairT ld_pk(const PairT* p, uint64_t pol) { return ld_pair(p, pol); }
-
+// Per-warp shared memory of the bound screen (bytes).
 template <int KT>
 struct BoundSmem {
-    static constexpr int kCap = KT / 2;  // touched clusters tracked before a dense sweep
-    // fold buffer | accumulators | touched list | term slots | term-at | touched count
-    static constexpr size_t per_warp = kWarp * sizeof(double) + KT * sizeof(float) + kCap * sizeof(uint16_t) +
-                                       kWarp * sizeof(uint4) + kWarp + 16;
+    static constexpr int kCap = KT / 4;  // touched clusters tracked before a dense sweep
+    static constexpr uint32_t o_acc = 0;                   // int32[KT] fixed-point accumulators
+    static constexpr uint32_t o_fold = o_acc + KT * 4;     // double[32] fold buffer
+    static constexpr uint32_t o_ts = o_fold + 32 * 8;      // uint2[32]: (pair base − first slot, x bits)
+    static constexpr uint32_t o_tl = o_ts + 32 * 8;        // u16[kCap] touched list
+    static constexpr uint32_t o_tat = o_tl + kCap * 2;     // u8[32] window slot -> term lane
+    static constexpr uint32_t o_cnt = o_tat + 32;          // u32 touched count
+    static constexpr size_t per_warp = o_cnt + 16;
 };
 
-template <int KT>
-__global__ void __launch_bounds__(256, 4) bound_screen_kernel(BoundArgs p) {
+__device__ __forceinline__ uint32_t sm_ld_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sm_st_u32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ uint2 sm_ld_u64(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sm_st_u64(uint32_t a, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(v.x), "r"(v.y));
+}
+__device__ __forceinline__ uint32_t sm_ld_u8(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sm_st_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)));
+}
+__device__ __forceinline__ uint32_t sm_ld_u16(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sm_st_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)));
+}
+__device__ __forceinline__ int sm_atom_add(uint32_t a, int v) {
+    int old;
+    asm volatile("atom.shared.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
+    return old;
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Fold the lanes' exact fp64 products of one chunk into s in ascending entry
+// order (every lane folds the same sequence: s is warp-uniform).
+__device__ __forceinline__ double fold_chunk(double s, double prod, int n, int lane, double* wsm) {
+    wsm[lane] = prod;
+    __syncwarp();
+    const double2* w2 = reinterpret_cast<const double2*>(wsm);
+    if (n == kWarp) {
+#pragma unroll
+        for (int j = 0; j < kWarp / 2; ++j) {
+            const double2 q = w2[j];
+            s += q.x;
+            s += q.y;
+        }
+    } else {
+        int j = 0;
+        for (; j + 2 <= n; j += 2) {
+            const double2 q = w2[j >> 1];
+            s += q.x;
+            s += q.y;
+        }
+        if (j < n) s += wsm[j];
+    }
+    __syncwarp();
+    return s;
+}
+
+// Candidate dot (rare: ~0.3 per document) kept out of line so its gather
+// arrays do not add to the screen loop's register pressure.
+#ifndef SSKM_CAND_INLINE
+#define SSKM_CAND_INLINE 1
+#endif
+#if SSKM_CAND_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+double cand_dot(const int32_t* __restrict__ idx, const float* __restrict__ val, int64_t beg,
+                                        int64_t end, const float* __restrict__ M, uint64_t ld, uint32_t col, int lane,
+                                        double* wsm) {
+    return doc_col_dot_sm(idx, val, beg, end, M, ld, col, lane, wsm);
+}
+
+// γ(n) = n·u/(1 − n·u) ≤ n·u·(1 + 2·n·u) for n·u ≤ 1/2 (no fp64 division).
+__device__ __forceinline__ double gamma_ub(double n, double u) {
+    const double nu = n * u;
+    return nu * (1.0 + 2.0 * nu);
+}
+
+// A warp per document, 32 entries (one chunk) at a time. The pipeline keeps
+// the next document's extents and start cluster one document ahead (its id two
+// ahead) and every chunk's (term, weight) one chunk ahead, across document
+// boundaries; per chunk, the terms' high-postings extents and own-column
+// weights are gathered together, then the chunk's high pairs are taken in
+// windows of 32 slots (one pair per lane) into the fixed-point accumulators
+// with shared integer atomics; the first touch of a cluster appends it to the
+// touched list.
+template <int KT, int INIT>
+__global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(BoundArgs p) {
     using SM = BoundSmem<KT>;
     constexpr int kCap = SM::kCap;
     extern __shared__ __align__(16) unsigned char smem_b[];
     const int lane = threadIdx.x & (kWarp - 1);
     const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
     unsigned char* base = smem_b + static_cast<size_t>(warp) * SM::per_warp;
-    double* fold = reinterpret_cast<double*>(base);
-    float* acc = reinterpret_cast<float*>(base + kWarp * sizeof(double));
-    uint16_t* tl = reinterpret_cast<uint16_t*>(base + kWarp * sizeof(double) + KT * sizeof(float));
-    uint4* ts = reinterpret_cast<uint4*>(base + kWarp * sizeof(double) + KT * sizeof(float) + kCap * sizeof(uint16_t));
-    uint8_t* term_at = reinterpret_cast<uint8_t*>(ts + kWarp);
-    uint32_t* ntouch_s = reinterpret_cast<uint32_t*>(term_at + kWarp);
-    const uint32_t acc_s = static_cast<uint32_t>(__cvta_generic_to_shared(acc));
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int c = lane * 4; c < KT; c += kWarp * 4) *reinterpret_cast<float4*>(acc + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(base));
+    double* fold = reinterpret_cast<double*>(base + SM::o_fold);
+    const uint32_t s_acc = sb + SM::o_acc, s_ts = sb + SM::o_ts, s_tl = sb + SM::o_tl, s_tat = sb + SM::o_tat,
+                   s_cnt = sb + SM::o_cnt;
+    for (int c = lane; c < KT; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
     __syncwarp();
-    const PairT* __restrict__ pairs = p.pairs;
+    const uint2* __restrict__ pairs = p.pairs;
     const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-    const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_list, gridDim.x));
+    const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_work, gridDim.x));
     const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
-    const int64_t w1 = imin64(p.n_list, w0 + chunk);
-    unsigned long long cands = 0, npairs = 0;
-    for (int64_t w = w0 + warp; w < w1; w += nwarps) {
-        const int64_t i = __ldg(p.list + w);
-        const int64_t beg = __ldg(p.indptr + i), end = __ldg(p.indptr + i + 1);
-        if (lane == 0) *ntouch_s = 0u;
-        __syncwarp();
-        // the running best's own column: its exact value is `best` already, and
-        // it is where most of a document's high pairs land — skipping it keeps
-        // the lanes' atomics apart
-        uint32_t own_l;
-        {
-            const uint32_t a0 = __ldg(p.a + i);
-            const uint32_t col = p.col_ids ? (a0 < p.k ? __ldg(p.col_of + a0) : kNone) : a0;
-            own_l = col - p.c0 < p.kt ? col - p.c0 : kNone;
+    const int64_t w1 = imin64(p.n_work, w0 + chunk);
+    const bool first = p.first != 0;
+    const unsigned lane_le = 0xFFFFFFFFu >> (31 - lane);
+    uint32_t cands = 0, npairs = 0, dnnz = 0, cnnz = 0, visits = 0, owns = 0;
+    auto doc_of = [&](int64_t ww) -> uint32_t { return p.order ? __ldg(p.order + ww) : static_cast<uint32_t>(ww); };
+    auto start_of = [&](uint32_t i) -> uint32_t {
+        if constexpr (INIT == kInitNcc) return first ? __ldg(p.a_start + i) : p.a[i];
+        return p.a[i];
+    };
+    int64_t w = w0 + warp;
+    uint32_t i_n = 0, i_nn = 0, arg_n = 0;
+    int64_t beg_n = 0, end_n = 0;
+    if (w < w1) {
+        i_n = doc_of(w);
+        beg_n = __ldg(p.indptr + i_n);
+        end_n = __ldg(p.indptr + i_n + 1);
+        arg_n = start_of(i_n);
+    }
+    if (w + nwarps < w1) i_nn = doc_of(w + nwarps);
+    int32_t t_n = 0;
+    float x_n = 0.f;
+    if (w < w1 && beg_n + lane < end_n) {
+        t_n = ld_stream_i32(p.idx + beg_n + lane, pol_stream);
+        x_n = ld_stream_f32(p.val + beg_n + lane, pol_stream);
+    }
+    for (; w < w1; w += nwarps) {
+        const uint32_t i = i_n;
+        const int64_t beg = beg_n, end = end_n;
+        uint32_t arg = arg_n;
+        const int64_t wn = w + nwarps;
+        if (wn < w1) {
+            i_n = i_nn;
+            beg_n = __ldg(p.indptr + i_n);
+            end_n = __ldg(p.indptr + i_n + 1);
+            arg_n = start_of(i_n);
         }
-        for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
-            const int64_t e = e0 + lane;
-            uint32_t lb = 0, le = 0;
-            float x = 0.f;
-            if (e < end) {
-                const int32_t t = ld_stream_i32(p.idx + e, pol_stream);
-                x = ld_stream_f32(p.val + e, pol_stream);
-                lb = __ldg(p.pptr + t);
-                le = __ldg(p.pptr + t + 1);
-            }
-            // the chunk's high pairs, flattened: 32-slot windows, one pair per
-            // lane (high lists are short, ~1.3 pairs per term on c1, so lanes
-            // stay busy). Slot s belongs to the term whose exclusive prefix is
-            // the last <= s. Lanes of different terms may meet the same cluster:
-            // shared float atomics (fp32 order then varies, which the bound
-            // tolerates; results never depend on it).
-            const uint32_t cnt = le - lb;
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int off = 1; off < kWarp; off <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-                if (lane >= off) incl += v;
-            }
-            const uint32_t excl = incl - cnt, total = __shfl_sync(0xFFFFFFFFu, incl, kWarp - 1);
-            npairs += cnt;
-            ts[lane] = make_uint4(lb, excl, __float_as_uint(x), 0u);
-            for (uint32_t base = 0; base < total; base += kWarp) {
-                uint32_t hb = 0;
-                if (cnt > 0 && excl < base + kWarp && excl + cnt > base) {
-                    const uint32_t pos = (excl > base ? excl : base) - base;  // this term's first slot here
-                    hb = 1u << pos;
-                    term_at[pos] = static_cast<uint8_t>(lane);
+        if (wn + nwarps < w1) i_nn = doc_of(wn + nwarps);
+        // baseline of this document (first tile), or the running state
+        bool active = true, need_dot = false;
+        double best = 0.0;
+        if (first) {
+            if constexpr (INIT == kInitFull) {
+                if (arg >= p.k) {
+                    best = -2.0;
+                } else {
+                    need_dot = p.same == nullptr || p.same[arg] == 0;
+                    if (!need_dot) best = p.sims[i];
                 }
-                const uint32_t heads = __reduce_or_sync(0xFFFFFFFFu, hb);
-                __syncwarp();
-                const uint32_t sl = base + lane;
-                if (sl < total) {
-                    const int ph = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
-                    const uint4 T = ts[term_at[ph]];
-                    const PairT pr = ld_pk(pairs + T.x + (sl - T.y), pol_keep);
-                    if (pr.x != own_l) {
-                        const float old = atomicAdd(acc + pr.x, __uint_as_float(T.z) * __uint_as_float(pr.y));
-                        if (old == 0.f) {  // first touch (an exact return to 0 only duplicates)
-                            const uint32_t pos = atomicAdd(ntouch_s, 1u);
-                            if (pos < static_cast<uint32_t>(kCap)) tl[pos] = static_cast<uint16_t>(pr.x);
+            } else if constexpr (INIT == kInitNcc) {
+                need_dot = p.unchanged[arg] == 0;
+                if (!need_dot) best = __ldg(p.sims_start + i);
+            } else {
+                best = p.sims[i];
+            }
+        } else {
+            active = p.take[w] != 0;
+            best = p.sims[i];
+        }
+        const float2 xb = __ldg(p.xb + i);
+        const uint32_t own_col = p.col_ids ? (arg < p.k ? __ldg(p.col_of + arg) : kNone) : arg;
+        const uint32_t own_l = own_col - p.c0 < p.kt ? own_col - p.c0 : kNone;
+        if (lane == 0) sm_st_u32(s_cnt, 0u);
+        __syncwarp();
+        double s_own = 0.0;
+        bool pref_done = false;
+        if (active) {
+            ++visits;
+            dnnz += static_cast<uint32_t>(end - beg);
+            for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
+                const bool valid = e0 + lane < end;
+                const int32_t t = t_n;
+                const float x = x_n;
+                // this chunk's postings extent and own-column weight
+                uint2 ext = make_uint2(0u, 0u);
+                float cv = 0.f;
+                if (valid) {
+                    ext = __ldg(p.hptr + t);
+                    if (need_dot) cv = __ldg(p.CT + static_cast<uint64_t>(t) * p.ld_ct + arg);
+                }
+                // the next chunk: this document's, else the next document's first
+                {
+                    const bool last = e0 + kWarp >= end;
+                    const int64_t en = last ? beg_n + lane : e0 + kWarp + lane;
+                    const int64_t lim = last ? (wn < w1 ? end_n : 0) : end;
+                    t_n = 0;
+                    x_n = 0.f;
+                    if (en < lim) {
+                        t_n = ld_stream_i32(p.idx + en, pol_stream);
+                        x_n = ld_stream_f32(p.val + en, pol_stream);
+                    }
+                    if (last) pref_done = true;
+                }
+                // slots: exclusive prefix of the terms' high-list lengths
+                const uint32_t cnt = ext.y;
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int off = 1; off < kWarp; off <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+                    if (lane >= off) incl += v;
+                }
+                const uint32_t excl = incl - cnt, total = __shfl_sync(0xFFFFFFFFu, incl, kWarp - 1);
+                npairs += total;
+                sm_st_u64(s_ts + 8u * lane, make_uint2(ext.x - excl, __float_as_uint(x)));
+                // windows of 32 slots, one pair per lane; slot s belongs to the
+                // term whose range holds it (the last head at or before s)
+                for (uint32_t wb = 0; wb < total; wb += kWarp) {
+                    uint32_t hb = 0;
+                    if (cnt > 0 && excl < wb + kWarp && excl + cnt > wb) {
+                        const uint32_t pos = excl > wb ? excl - wb : 0u;
+                        hb = 1u << pos;
+                        sm_st_u8(s_tat + pos, static_cast<uint32_t>(lane));
+                    }
+                    const uint32_t heads = __reduce_or_sync(0xFFFFFFFFu, hb);
+                    __syncwarp();
+                    const uint32_t sl = wb + lane;
+                    if (sl < total) {
+                        const int ph = 31 - __clz(heads & lane_le);
+                        const uint2 en = sm_ld_u64(s_ts + 8u * sm_ld_u8(s_tat + ph));
+                        const uint2 pr = ld_pair(pairs + (en.x + sl), pol_keep);
+                        if (pr.x != own_l) {
+                            const int qv = __float2int_rn(__uint_as_float(en.y) * __uint_as_float(pr.y) * kFixScale);
+                            if (qv != 0) {
+                                const int old = sm_atom_add(s_acc + 4u * pr.x, qv);
+                                if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
+                                    const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
+                                    if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr.x);
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (need_dot)  // own dot, ascending entry order, exact in fp64
+                    s_own = fold_chunk(s_own, static_cast<double>(x) * static_cast<double>(cv),
+                                       static_cast<int>(imin64(kWarp, end - e0)), lane, fold);
+            }
+        }
+        if (!pref_done) {  // empty or skipped document: prefetch the next one's first chunk
+            t_n = 0;
+            x_n = 0.f;
+            if (wn < w1 && beg_n + lane < end_n) {
+                t_n = ld_stream_i32(p.idx + beg_n + lane, pol_stream);
+                x_n = ld_stream_f32(p.val + beg_n + lane, pol_stream);
+            }
+        }
+        __syncwarp();
+        const uint32_t ntouch = sm_ld_u32(s_cnt);
+        const double nn = static_cast<double>(end - beg);
+        const double g32 = gamma_ub(nn + 32.0, 0x1p-24), g64 = gamma_ub(nn, 0x1p-53);
+        const double tiny = nn * kFixUnit + nn * 0x1p-126;
+        if (first && active) {
+            if (need_dot) {
+                best = s_own;
+                ++owns;
+            }
+            // no cluster without a high entry shared with x can exceed lb
+            const double lb = p.theta * xb.x * (1.0 + 1e-12) + g64 * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
+            const bool take = best > lb && (INIT != kInitFull || arg < p.k);
+            if (lane == 0) {
+                p.take[w] = take ? 1 : 0;
+                if (!take) {
+                    const unsigned long long pos = atomicAdd(p.n_exact, 1ull);
+                    p.exact_list[pos] = i;
+                }
+            }
+            active = take;
+        }
+        const bool dense = ntouch > static_cast<uint32_t>(kCap);
+        if (active) {
+            // candidates: touched clusters whose upper bound reaches the running best
+            const double bx = p.theta * xb.x * (1.0 + 1e-12) + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
+            const uint32_t count = dense ? p.kt : ntouch;
+            for (uint32_t k0 = 0; k0 < count; k0 += kWarp) {
+                const uint32_t kk = k0 + lane;
+                bool cand = false;
+                uint32_t gid = 0;
+                double ub = 0.0;
+                if (kk < count) {
+                    const uint32_t jl = dense ? kk : sm_ld_u16(s_tl + 2u * kk);
+                    gid = p.col_ids ? __ldg(p.col_ids + p.c0 + jl) : p.c0 + jl;
+                    ub = static_cast<double>(static_cast<int>(sm_ld_u32(s_acc + 4u * jl))) * kFixUnit + bx;
+                    cand = gid != arg && ub >= best;
+                }
+                unsigned cm = __ballot_sync(0xFFFFFFFFu, cand);
+                while (cm) {
+                    const int src = __ffs(cm) - 1;
+                    cm &= cm - 1;
+                    const uint32_t g = __shfl_sync(0xFFFFFFFFu, gid, src);
+                    const double u = __shfl_sync(0xFFFFFFFFu, ub, src);
+                    if (u >= best) {  // best only grows: re-check
+                        const double s = cand_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, g, lane, fold);
+                        ++cands;
+                        cnnz += static_cast<uint32_t>(end - beg);
+                        if (s > best || (s == best && g < arg)) {
+                            best = s;
+                            arg = g;
                         }
                     }
                 }
-                __syncwarp();
+            }
+            if (lane == 0) {
+                p.a[i] = arg;
+                p.sims[i] = best;
             }
         }
+        // clear the touched accumulators
         __syncwarp();
-        const uint32_t ntouch = *ntouch_s;
-        // candidates: touched clusters whose upper bound reaches the running best
-        double best = p.sims[i];
-        uint32_t arg = p.a[i];
-        const double q = __ldg(p.xnorm2 + i);
-        const double nn = static_cast<double>(end - beg);
-        const double u32 = 0x1p-24, u64 = 0x1p-53;
-        const double n32 = nn + 32.0;
-        const double g32 = n32 * u32 / (1.0 - n32 * u32), g64 = nn * u64 / (1.0 - nn * u64);
-        const double bx = p.theta * __ldg(p.xnorm1 + i) * (1.0 + 1e-12) +
-                          (g32 + g64) * sqrt(q) * p.cmax * (1.0 + 1e-12) + nn * 0x1p-126;
-        const bool dense = ntouch > static_cast<uint32_t>(kCap);
-        const uint32_t count = dense ? p.kt : ntouch;
-        for (uint32_t c0 = 0; c0 < count; c0 += kWarp) {
-            const uint32_t k = c0 + lane;
-            bool cand = false;
-            uint32_t gid = 0;
-            double ub = 0.0;
-            if (k < count) {
-                const uint32_t jl = dense ? k : tl[k];
-                const float v = lds_f32(acc_s + jl * 4u);
-                gid = p.col_ids ? __ldg(p.col_ids + p.c0 + jl) : p.c0 + jl;
-                ub = static_cast<double>(v) + bx;
-                cand = gid != arg && ub >= best;
-            }
-            unsigned cm = __ballot_sync(0xFFFFFFFFu, cand);
-            while (cm) {
-                const int src = __ffs(cm) - 1;
-                cm &= cm - 1;
-                const uint32_t g = __shfl_sync(0xFFFFFFFFu, gid, src);
-                const double u = __shfl_sync(0xFFFFFFFFu, ub, src);
-                if (u >= best) {  // best only grows: re-check
-                    const double s = doc_col_dot_sm(p.idx, p.val, beg, end, p.CT, p.ld_ct, g, lane, fold);
-                    ++cands;
-                    if (s > best || (s == best && g < arg)) {
-                        best = s;
-                        arg = g;
-                    }
+        if (dense) {
+            for (int c = lane; c < KT; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
+        } else {
+            for (uint32_t kk = lane; kk < ntouch; kk += kWarp) sm_st_u32(s_acc + 4u * sm_ld_u16(s_tl + 2u * kk), 0u);
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        atomicAdd(p.n_cand, static_cast<unsigned long long>(cands));
+        atomicAdd(p.n_doc_nnz, static_cast<unsigned long long>(dnnz));
+        atomicAdd(p.n_cand_nnz, static_cast<unsigned long long>(cnnz));
+        atomicAdd(p.n_visits, static_cast<unsigned long long>(visits));
+        atomicAdd(p.n_own, static_cast<unsigned long long>(owns));
+        atomicAdd(p.n_pairs, static_cast<unsigned long long>(npairs));
+    }
+}
+
+// High postings of the cluster tile [c0, c0 + kt) of M in one pass over M:
+// per term, the (column, value) pairs with |value| ≥ thr in ascending column,
+// at a block-reserved offset (one atomic per 8 terms). Lists land in any order;
+// hptr[t] = (first pair, count). Pairs beyond `cap` are not written (the host
+// grows the buffer and rebuilds when *total > cap).
+__global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
+                                                           uint32_t c0, uint32_t kt, float thr,
+                                                           uint2* __restrict__ hptr, uint2* __restrict__ pairs,
+                                                           unsigned long long cap, unsigned long long* total) {
+    __shared__ uint32_t s_cnt[8];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x / kWarp;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint64_t tb = static_cast<uint64_t>(blockIdx.x) * 8; tb < d; tb += static_cast<uint64_t>(gridDim.x) * 8) {
+        const uint64_t t = tb + warp;
+        const float* row = M + t * ld + c0;
+        uint32_t cnt = 0;
+        if (t < d)
+            for (uint32_t j = lane; j < kt; j += kWarp) cnt += post_keep(row[j], thr);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
+        if (lane == 0) s_cnt[warp] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sum += s_cnt[q];
+            s_base = sum ? atomicAdd(total, static_cast<unsigned long long>(sum)) : 0ull;
+        }
+        __syncthreads();
+        unsigned long long b = s_base;
+        for (int q = 0; q < warp; ++q) b += s_cnt[q];
+        if (t < d) {
+            if (lane == 0) hptr[t] = make_uint2(static_cast<uint32_t>(b), cnt);
+            if (cnt > 0 && b + cnt <= cap) {
+                uint32_t run = 0;
+                for (uint32_t j0 = 0; j0 < kt; j0 += kWarp) {
+                    const uint32_t j = j0 + lane;
+                    const float v = j < kt ? row[j] : 0.f;
+                    const bool keep = j < kt && post_keep(v, thr);
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+                    if (keep) pairs[b + run + __popc(m & lt)] = make_uint2(j, __float_as_uint(v));
+                    run += __popc(m);
+                    if (run == cnt) break;
                 }
             }
         }
-        __syncwarp();
-        if (dense) {
-            for (int c = lane * 4; c < KT; c += kWarp * 4)
-                *reinterpret_cast<float4*>(acc + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-            for (uint32_t k = lane; k < ntouch; k += kWarp) sts_f32(acc_s + tl[k] * 4u, 0.f);
-        }
-        __syncwarp();
-        if (lane == 0) {
-            p.a[i] = arg;
-            p.sims[i] = best;
-        }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) npairs += __shfl_xor_sync(0xFFFFFFFFu, npairs, off);  // per-lane terms
-    if (lane == 0) {
-        atomicAdd(p.n_cand, cands);
-        atomicAdd(p.n_pairs, npairs);
+        __syncthreads();  // s_cnt / s_base reuse
     }
 }
 
 // NCC pass A over the bound-screened documents: queue the rescan exactly as
 // the reference decides it (engine.cpp:303-305); the exact-scan documents
 // queue themselves in assign_tile_kernel.
-__global__ void bound_ncc_rescan_kernel(const uint32_t* __restrict__ list, int64_t n_list,
-                                        const uint32_t* __restrict__ a_start, const double* __restrict__ sims_start,
-                                        const double* __restrict__ sims, const uint8_t* __restrict__ unchanged,
-                                        uint32_t* __restrict__ rescan_list, unsigned long long* n_rescan) {
-    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < n_list;
+__global__ void bound_ncc_rescan_kernel(const uint32_t* __restrict__ order, int64_t n_work,
+                                        const uint8_t* __restrict__ take, const uint32_t* __restrict__ a_start,
+                                        const double* __restrict__ sims_start, const double* __restrict__ sims,
+                                        const uint8_t* __restrict__ unchanged, uint32_t* __restrict__ rescan_list,
+                                        unsigned long long* n_rescan) {
+    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < n_work;
          w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t i = list[w];
+        if (!take[w]) continue;
+        const uint32_t i = order ? order[w] : static_cast<uint32_t>(w);
         if (unchanged[a_start[i]] == 0 && !(sims[i] > sims_start[i])) {
             const unsigned long long pos = atomicAdd(n_rescan, 1ull);
             rescan_list[pos] = i;
@@ -296,9 +495,10 @@ __global__ void bound_ncc_rescan_kernel(const uint32_t* __restrict__ list, int64
     }
 }
 
-// ‖x‖₁ per document (fp64), once per upload.
-__global__ void doc_norm1_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ val, int64_t n,
-                                 double* __restrict__ out) {
+// Per-document bound inputs, once per upload: (‖x‖₁, ‖x‖₂) rounded up to fp32
+// (rounding up keeps every bound valid; one 8-byte load per document).
+__global__ void doc_bound_norms_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ val, int64_t n,
+                                       const double* __restrict__ xnorm2, float2* __restrict__ out) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
@@ -307,9 +507,11 @@ __global__ void doc_norm1_kernel(const int64_t* __restrict__ indptr, const float
         for (int64_t e = indptr[i] + lane; e < indptr[i + 1]; e += kWarp) q += fabs(static_cast<double>(val[e]));
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, off);
-        // upper bound: the fp64 sum's rounding (< n·2^-53 relative) covered
-        const double n = static_cast<double>(indptr[i + 1] - indptr[i]);
-        if (lane == 0) out[i] = q * (1.0 + (n + 2.0) * 0x1p-52);
+        // the fp64 sums' rounding (< (n + 2)·2^-53 relative) covered
+        const double m = static_cast<double>(indptr[i + 1] - indptr[i]);
+        const double x1 = q * (1.0 + (m + 2.0) * 0x1p-52);
+        const double x2 = sqrt(xnorm2[i] * (1.0 + (m + 2.0) * 0x1p-52)) * (1.0 + 0x1p-50);
+        if (lane == 0) out[i] = make_float2(__double2float_ru(x1), __double2float_ru(x2));
     }
 }
 

@@ -181,8 +181,8 @@ public:
         nonneg_ = (hs_->bad & 16u) == 0;
         xnorm2_.alloc(n);
         launch(doc_norm2_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p);
-        xnorm1_.alloc(n);
-        launch(doc_norm1_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm1_.p);
+        xb_.alloc(n);
+        launch(doc_bound_norms_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p, xb_.p);
         CK_LAUNCH();
         // fixed-point scale: N_total · 2^K <= 2^62 with |x| <= 1
         int lg = 0;
@@ -234,6 +234,7 @@ public:
         unchanged_.alloc(k_);
         touched_.alloc(k_);
         repaired_flag_.alloc(k_);
+        same_.alloc(k_);
         counts_.alloc(k_);
         rec_ids_.alloc(k_);
         rec_pos_.alloc(k_);
@@ -1107,9 +1108,10 @@ private:
         }
         launch(flags_kernel, grid_for(k_, 256), 256, 
             k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon, touched_.p, repaired_flag_.p, rec_pos_.p,
-            drift_rec_.p, unchanged_.p, drift_.p, &scal_.p->max_drift_bits, &scal_.p->n_unchanged);
+            drift_rec_.p, unchanged_.p, same_.p, drift_.p, &scal_.p->max_drift_bits, &scal_.p->n_unchanged);
         CK_LAUNCH();
         CK(cudaMemsetAsync(touched_.p, 0, k_, stream_));
+        ++updates_since_assign_;
         pull_scalars();
         if (hs_->zero_flag) throw InvalidArgument("cannot normalize zero vector");
         n_unchanged_ = hs_->n_unchanged;
@@ -1146,6 +1148,8 @@ private:
     void snapshot_start() {
         screen_ms_ = 0.0;
         screen_launches_ = 0;
+        bstat_docs_ = bstat_pairs_ = bstat_cand_ = bstat_doc_nnz_ = bstat_cand_nnz_ = bstat_visits_ = bstat_own_ = 0;
+        bstat_theta_ = 0.0;
         CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
         CK(cudaMemcpyAsync(sims_start_.p, sims_.p, n_ * 8, cudaMemcpyDeviceToDevice, stream_));
     }
@@ -1222,123 +1226,95 @@ private:
     void bound_assign(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* order,
                       int64_t n_work, int init) {
         btake_.alloc(n_);
-        bwork_.alloc(n_);
-        bctr_.alloc(4);
-        CK(cudaMemsetAsync(bctr_.p, 0, 4 * sizeof(unsigned long long), stream_));
+        bctr_.alloc(8);
+        CK(cudaMemsetAsync(bctr_.p, 0, 8 * sizeof(unsigned long long), stream_));
         const float thr = theta_;
-        BoundInitArgs ia{};
-        ia.indptr = indptr_.p;
-        ia.idx = idx_.p;
-        ia.val = val_.p;
-        ia.CT = ct_.p;
-        ia.ld_ct = ld_;
-        ia.order = order;
-        ia.n_work = n_work;
-        ia.xnorm2 = xnorm2_.p;
-        ia.xnorm1 = xnorm1_.p;
-        ia.theta = static_cast<double>(thr);
-        ia.cmax = cmax_;
-        ia.k = k_;
-        ia.a = a_.p;
-        ia.sims = sims_.p;
-        ia.unchanged = unchanged_.p;
-        ia.a_start = a_start_.p;
-        ia.sims_start = sims_start_.p;
-        ia.take = btake_.p;
-        ia.exact_list = exact_.p;
-        ia.n_exact = &scal_.p->n_exact;
-        if (init == kInitFull)
-            launch(bound_init_kernel<kInitFull>, grid_for(n_work * 32, 256), 256, ia);
-        else if (init == kInitNcc)
-            launch(bound_init_kernel<kInitNcc>, grid_for(n_work * 32, 256), 256, ia);
-        else
-            launch(bound_init_kernel<kInitRescan>, grid_for(n_work * 32, 256), 256, ia);
-        CK_LAUNCH();
-        // documents taken by the bound screen, in work-list (cluster) order
-        size_t tmp = 0;
-        cub::CountingInputIterator<uint32_t> iota(0);
-        if (order) {
-            CK(cub::DeviceSelect::Flagged(nullptr, tmp, order, btake_.p, bwork_.p, bctr_.p + 3,
-                                          static_cast<int>(n_work), stream_));
-            grow_tmp(tmp);
-            CK(cub::DeviceSelect::Flagged(bsel_tmp_.p, tmp, order, btake_.p, bwork_.p, bctr_.p + 3,
-                                          static_cast<int>(n_work), stream_));
-        } else {
-            CK(cub::DeviceSelect::Flagged(nullptr, tmp, iota, btake_.p, bwork_.p, bctr_.p + 3,
-                                          static_cast<int>(n_work), stream_));
-            grow_tmp(tmp);
-            CK(cub::DeviceSelect::Flagged(bsel_tmp_.p, tmp, iota, btake_.p, bwork_.p, bctr_.p + 3,
-                                          static_cast<int>(n_work), stream_));
+        const uint32_t KT = ncols <= 1024 ? 1024 : 2048;
+        BoundArgs p{};
+        p.indptr = indptr_.p;
+        p.idx = idx_.p;
+        p.val = val_.p;
+        p.col_ids = col_ids;
+        p.order = order;
+        p.n_work = n_work;
+        p.CT = ct_.p;
+        p.ld_ct = ld_;
+        p.xb = xb_.p;
+        p.theta = static_cast<double>(thr);
+        p.cmax = cmax_;
+        p.k = k_;
+        p.a = a_.p;
+        p.sims = sims_.p;
+        p.unchanged = unchanged_.p;
+        // the cached similarity of a full-scan document is exact for its
+        // cluster when that column is bit-identical to the one the cache was
+        // computed against (one update since this engine's last assign)
+        p.same = (init == kInitFull && cache_trusted_ && updates_since_assign_ == 1 && iteration_ >= 2) ? same_.p
+                                                                                                        : nullptr;
+        p.a_start = a_start_.p;
+        p.sims_start = sims_start_.p;
+        p.take = btake_.p;
+        p.exact_list = exact_.p;
+        p.n_exact = &scal_.p->n_exact;
+        p.n_cand = bctr_.p + 0;
+        p.n_pairs = bctr_.p + 1;
+        p.n_visits = bctr_.p + 2;
+        p.n_own = bctr_.p + 3;
+        p.n_doc_nnz = bctr_.p + 4;
+        p.n_cand_nnz = bctr_.p + 5;
+        if (col_ids) {  // cluster -> column of M
+            bcol_of_.alloc(k_);
+            launch(fill_u32_kernel, grid_for(k_, 256), 256, bcol_of_.p, static_cast<int64_t>(k_), kNone);
+            launch(scatter_pos_kernel, grid_for(ncols, 256), 256, col_ids, ncols, bcol_of_.p);
+            p.col_of = bcol_of_.p;
         }
-        ++launches_;
-        unsigned long long n_list = 0;
-        CK(cudaMemcpyAsync(&n_list, bctr_.p + 3, 8, cudaMemcpyDeviceToHost, stream_));
-        CK(cudaStreamSynchronize(stream_));
-        if (n_list > 0) {
-            const uint32_t KT = ncols <= 1024 ? 1024 : 2048;
-            BoundArgs p{};
-            p.indptr = indptr_.p;
-            p.idx = idx_.p;
-            p.val = val_.p;
-            p.col_ids = col_ids;
-            p.list = bwork_.p;
-            p.n_list = static_cast<int64_t>(n_list);
-            p.CT = ct_.p;
-            p.ld_ct = ld_;
-            p.xnorm2 = xnorm2_.p;
-            p.xnorm1 = xnorm1_.p;
-            p.theta = static_cast<double>(thr);
-            p.cmax = cmax_;
-            p.a = a_.p;
-            p.sims = sims_.p;
-            p.n_cand = bctr_.p + 0;
-            p.n_pairs = bctr_.p + 1;
-            p.k = k_;
-            if (col_ids) {  // cluster -> column of M
-                bcol_of_.alloc(k_);
-                launch(fill_u32_kernel, grid_for(k_, 256), 256, bcol_of_.p, static_cast<int64_t>(k_), kNone);
-                launch(scatter_pos_kernel, grid_for(ncols, 256), 256, col_ids, ncols, bcol_of_.p);
-                p.col_of = bcol_of_.p;
-            }
-            for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
-                const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
-                build_postings(M, ld, c0, kt, thr);
-                p.pptr = pptr_.p;
-                p.pairs = pairs_.p;
-                p.c0 = c0;
-                p.kt = kt;
-                CK(cudaEventRecord(ev_[6], stream_));
-                if (KT == 1024)
-                    bound_launch<1024>(p);
-                else
-                    bound_launch<2048>(p);
-                CK(cudaEventRecord(ev_[7], stream_));
-                CK(cudaEventSynchronize(ev_[7]));
-                float ms = 0.f;
-                CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
-                screen_ms_ += ms;
-                screen_launches_ += 1;
-            }
-            if (init == kInitNcc)
-                launch(bound_ncc_rescan_kernel, grid_for(static_cast<int64_t>(n_list), 256), 256, bwork_.p,
-                       static_cast<int64_t>(n_list), a_start_.p, sims_start_.p, sims_.p, unchanged_.p, rescan_.p,
-                       &scal_.p->n_rescan);
+        for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
+            const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
+            build_hipost(M, ld, c0, kt, thr);
+            p.hptr = hptr_.p;
+            p.pairs = pairs_.p;
+            p.c0 = c0;
+            p.kt = kt;
+            p.first = c0 == 0 ? 1 : 0;
+            CK(cudaEventRecord(ev_[6], stream_));
+            if (KT == 1024)
+                bound_launch<1024>(p, init);
+            else
+                bound_launch<2048>(p, init);
+            CK(cudaEventRecord(ev_[7], stream_));
+            CK(cudaEventSynchronize(ev_[7]));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
+            screen_ms_ += ms;
+            screen_launches_ += 1;
         }
+        if (init == kInitNcc)
+            launch(bound_ncc_rescan_kernel, grid_for(n_work, 256), 256, order, n_work, btake_.p, a_start_.p,
+                   sims_start_.p, sims_.p, unchanged_.p, rescan_.p, &scal_.p->n_rescan);
         // θ for the next assign: keep the exact-scan share small and the
         // candidate dots near one per document (θ never changes a result)
-        unsigned long long ctr[2] = {0, 0};
+        unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
         uint64_t n_fb = 0;
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(&n_fb, &scal_.p->n_exact, 8, cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
-        last_bound_cand_ = ctr[0];
-        last_bound_pairs_ = ctr[1];
-        last_bound_list_ = n_list;
+        const uint64_t n_list = n_work > 0 ? static_cast<uint64_t>(n_work) - std::min<uint64_t>(n_fb, n_work) : 0;
+        bstat_docs_ += n_list;
+        bstat_pairs_ += ctr[1];
+        bstat_cand_ += ctr[0];
+        bstat_visits_ += ctr[2];
+        bstat_own_ += ctr[3];
+        bstat_doc_nnz_ += ctr[4];
+        bstat_cand_nnz_ += ctr[5];
+        bstat_theta_ = static_cast<double>(thr);
         if (debug_)
-            std::fprintf(stderr, "[sskm] bound init=%d theta=%.5g work=%lld list=%llu exact=%llu cand=%llu pairs=%llu\n",
+            std::fprintf(stderr,
+                         "[sskm] bound init=%d theta=%.5g work=%lld exact=%llu cand=%llu pairs=%llu own=%llu "
+                         "cache=%d\n",
                          init, static_cast<double>(thr), static_cast<long long>(n_work),
-                         static_cast<unsigned long long>(n_list), static_cast<unsigned long long>(n_fb),
-                         static_cast<unsigned long long>(ctr[0]), static_cast<unsigned long long>(ctr[1]));
+                         static_cast<unsigned long long>(n_fb), static_cast<unsigned long long>(ctr[0]),
+                         static_cast<unsigned long long>(ctr[1]), static_cast<unsigned long long>(ctr[3]),
+                         p.same != nullptr);
         if (theta_adapt_ && n_work > 0) {
             const double fb = static_cast<double>(n_fb) / static_cast<double>(n_work);
             const double cpd = n_list ? static_cast<double>(ctr[0]) / static_cast<double>(n_list) : 0.0;
@@ -1351,9 +1327,17 @@ private:
     }
 
     template <int KT>
-    void bound_launch(const BoundArgs& p) {
-        auto k = bound_screen_kernel<KT>;
-        const size_t per_warp = BoundSmem<KT>::per_warp;
+    void bound_launch(const BoundArgs& p, int init) {
+        if (init == kInitFull)
+            bound_launch_k(bound_screen_kernel<KT, kInitFull>, BoundSmem<KT>::per_warp, p);
+        else if (init == kInitNcc)
+            bound_launch_k(bound_screen_kernel<KT, kInitNcc>, BoundSmem<KT>::per_warp, p);
+        else
+            bound_launch_k(bound_screen_kernel<KT, kInitRescan>, BoundSmem<KT>::per_warp, p);
+    }
+
+    template <typename K>
+    void bound_launch_k(K k, size_t per_warp, const BoundArgs& p) {
         const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (100u << 10) / per_warp)));
         const size_t smem = static_cast<size_t>(warps) * per_warp;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1361,14 +1345,31 @@ private:
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem));
         per_sm = std::max(1, per_sm);
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(p.n_list, warps))));
+            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(p.n_work, warps))));
         k<<<grid, warps * 32, smem, stream_>>>(p);
         ++launches_;
         CK_LAUNCH();
     }
 
-    void grow_tmp(size_t n) {
-        if (n > bsel_tmp_.n) bsel_tmp_.alloc(n + n / 4 + 256);
+    // High postings (|value| >= thr) of the columns [c0, c0 + kt) of M into
+    // hptr_ / pairs_ in one pass over M; grows the pair buffer and rebuilds
+    // when the previous capacity was exceeded.
+    void build_hipost(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr) {
+        hptr_.alloc(d_);
+        hpctr_.alloc(1);
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 8));
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            CK(cudaMemsetAsync(hpctr_.p, 0, sizeof(unsigned long long), stream_));
+            launch(hipost_build_kernel, grid, 256, M, ld, d_, c0, kt, thr, hptr_.p, pairs_.p,
+                   static_cast<unsigned long long>(pairs_.n), hpctr_.p);
+            CK_LAUNCH();
+            unsigned long long total = 0;
+            CK(cudaMemcpyAsync(&total, hpctr_.p, 8, cudaMemcpyDeviceToHost, stream_));
+            CK(cudaStreamSynchronize(stream_));
+            if (total <= pairs_.n) return;
+            if (total >= (1ull << 32)) throw std::runtime_error("bound screen: high postings exceed 2^32 pairs");
+            pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
+        }
     }
 
     bool screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
@@ -1651,6 +1652,7 @@ private:
         pull_scalars();
         st->n_reassigned = hs_->reassigned;
         st->objective = hs_->objective;
+        updates_since_assign_ = 0;
     }
 
     void reset_scalars_keep_rescan() {
@@ -1667,6 +1669,14 @@ private:
         st->screen_ms = screen_ms_;
         st->screen_launches = screen_launches_;
         st->centroid_density = last_density_;
+        st->bound_docs = bstat_docs_;
+        st->bound_pairs = bstat_pairs_;
+        st->bound_candidates = bstat_cand_;
+        st->bound_doc_nnz = bstat_doc_nnz_;
+        st->bound_cand_nnz = bstat_cand_nnz_;
+        st->bound_theta = bstat_theta_;
+        st->bound_visits = bstat_visits_;
+        st->bound_own_dots = bstat_own_;
     }
 
     int device_;
@@ -1698,11 +1708,11 @@ private:
     DevBuf<int64_t> indptr_;
     DevBuf<int32_t> idx_;
     DevBuf<float> val_;
-    DevBuf<double> xnorm1_;
-    DevBuf<uint8_t> btake_;
-    DevBuf<uint32_t> bwork_, bcol_of_;
-    DevBuf<unsigned long long> bctr_;
-    DevBuf<unsigned char> bsel_tmp_;
+    DevBuf<float2> xb_;
+    DevBuf<uint8_t> btake_, same_;
+    DevBuf<uint32_t> bcol_of_;
+    DevBuf<uint2> hptr_;
+    DevBuf<unsigned long long> bctr_, hpctr_;
     // ncc+index accounting (index_account)
     DevBuf<uint32_t> ix_cnt_, ix_mval_, ix_jlen_, ix_lcnt_, ix_lptr_, ix_fill_, ix_list_;
     DevBuf<uint64_t> ix_off_, ix_cptr_, ix_keys_;
@@ -1733,7 +1743,11 @@ private:
     bool theta_adapt_ = true;
     bool debug_ = false;  // SSKM_DEBUG=1: per-assign screen counters on stderr
     float theta_ = 0.004f;        // high/low split of the centroid weights (SSKM_THETA)
-    uint64_t last_bound_cand_ = 0, last_bound_pairs_ = 0, last_bound_list_ = 0;  // measured: fusing costs the screen occupancy (c1 13.3 -> 18.0 ms)
+    // per-assign bound-screen totals (stats)
+    uint64_t bstat_docs_ = 0, bstat_pairs_ = 0, bstat_cand_ = 0, bstat_doc_nnz_ = 0, bstat_cand_nnz_ = 0,
+             bstat_visits_ = 0, bstat_own_ = 0;
+    uint32_t updates_since_assign_ = 0;  // updates since the last assign (the same_ flags' validity)
+    double bstat_theta_ = 0.0;
     bool nonneg_ = true;
     double last_density_ = 0.0;
     double dense_above_ = 0.15;
@@ -1819,6 +1833,14 @@ void step(Engine& e, sskm_iteration_stats* st) {
     st->index_queries = a.index_queries;
     st->candidates_total = a.candidates_total;
     st->index_build_seconds = a.index_build_seconds;
+    st->bound_docs = a.bound_docs;
+    st->bound_pairs = a.bound_pairs;
+    st->bound_candidates = a.bound_candidates;
+    st->bound_doc_nnz = a.bound_doc_nnz;
+    st->bound_cand_nnz = a.bound_cand_nnz;
+    st->bound_theta = a.bound_theta;
+    st->bound_visits = a.bound_visits;
+    st->bound_own_dots = a.bound_own_dots;
     st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 }  // namespace

@@ -278,15 +278,19 @@ __global__ void apply_moves_kernel(const uint32_t* __restrict__ pairs, uint32_t 
 
 // unchanged flags (detect_unchanged + repaired-forces-changed + iteration-1
 // rule, engine.cpp:366-376) and max drift.
+// same[j]: column j is bit-identical to its value before this update (not
+// rewritten, or rewritten with zero drift: Σ(new − old)² = 0 in fp64 of fp32
+// differences only for equal columns) — the bound screen's cached-similarity test.
 __global__ void flags_kernel(uint32_t k, int first_iter, double eps, const uint8_t* __restrict__ touched,
                              const uint8_t* __restrict__ repaired, const uint32_t* __restrict__ rec_pos,
                              const double* __restrict__ drift_rec, uint8_t* __restrict__ unchanged,
-                             double* __restrict__ drift_out, unsigned long long* max_drift_bits,
-                             unsigned int* n_unchanged) {
+                             uint8_t* __restrict__ same, double* __restrict__ drift_out,
+                             unsigned long long* max_drift_bits, unsigned int* n_unchanged) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
         double dj = 0.0;
         if (touched[j]) dj = drift_rec[rec_pos[j]];
         drift_out[j] = dj;
+        same[j] = (!first_iter && !repaired[j] && dj == 0.0) ? 1 : 0;
         uint8_t u;
         if (first_iter) {
             u = 0;
