@@ -103,8 +103,8 @@ class ClockSampler:
 
 
 def ncu_traffic():
-    """Per-launch DRAM bytes of the assign kernel from the committed ncu summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_assign_summary.json")
+    """Per-launch DRAM bytes of the bound screen from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_bound_summary.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)

@@ -79,10 +79,8 @@ struct BoundSmem {
     static constexpr int kCap = KT / 4;  // touched clusters tracked before a dense sweep
     static constexpr uint32_t o_acc = 0;                   // int32[KT] fixed-point accumulators
     static constexpr uint32_t o_fold = o_acc + KT * 4;     // double[32] fold buffer
-    static constexpr uint32_t o_ts = o_fold + 32 * 8;      // uint2[32]: (pair base − first slot, x bits)
-    static constexpr uint32_t o_tl = o_ts + 32 * 8;        // u16[kCap] touched list
-    static constexpr uint32_t o_tat = o_tl + kCap * 2;     // u8[32] window slot -> term lane
-    static constexpr uint32_t o_cnt = o_tat + 32;          // u32 touched count
+    static constexpr uint32_t o_tl = o_fold + 32 * 8;      // u16[kCap] touched list
+    static constexpr uint32_t o_cnt = o_tl + kCap * 2;     // u32 touched count
     static constexpr size_t per_warp = o_cnt + 16;
 };
 
@@ -193,8 +191,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     unsigned char* base = smem_b + static_cast<size_t>(warp) * SM::per_warp;
     const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(base));
     double* fold = reinterpret_cast<double*>(base + SM::o_fold);
-    const uint32_t s_acc = sb + SM::o_acc, s_ts = sb + SM::o_ts, s_tl = sb + SM::o_tl, s_tat = sb + SM::o_tat,
-                   s_cnt = sb + SM::o_cnt;
+    const uint32_t s_acc = sb + SM::o_acc, s_tl = sb + SM::o_tl, s_cnt = sb + SM::o_cnt;
     for (int c = lane; c < KT; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
     __syncwarp();
     const uint2* __restrict__ pairs = p.pairs;
@@ -203,7 +200,6 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
     const int64_t w1 = imin64(p.n_work, w0 + chunk);
     const bool first = p.first != 0;
-    const unsigned lane_le = 0xFFFFFFFFu >> (31 - lane);
     uint32_t cands = 0, npairs = 0, dnnz = 0, cnnz = 0, visits = 0, owns = 0;
     auto doc_of = [&](int64_t ww) -> uint32_t { return p.order ? __ldg(p.order + ww) : static_cast<uint32_t>(ww); };
     auto start_of = [&](uint32_t i) -> uint32_t {
@@ -293,46 +289,32 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     }
                     if (last) pref_done = true;
                 }
-                // slots: exclusive prefix of the terms' high-list lengths
+                // the term's high pairs, up to 4 per round with their loads in
+                // flight together (lists average ~1 pair on the TF-IDF corpora);
+                // longer lists loop on in the lanes that have them
                 const uint32_t cnt = ext.y;
-                uint32_t incl = cnt;
+                npairs += cnt;
+                const float xs = x * kFixScale;
+                for (uint32_t k0 = 0; k0 < cnt; k0 += 4) {
+                    uint2 pr[4];
 #pragma unroll
-                for (int off = 1; off < kWarp; off <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-                    if (lane >= off) incl += v;
-                }
-                const uint32_t excl = incl - cnt, total = __shfl_sync(0xFFFFFFFFu, incl, kWarp - 1);
-                npairs += total;
-                sm_st_u64(s_ts + 8u * lane, make_uint2(ext.x - excl, __float_as_uint(x)));
-                // windows of 32 slots, one pair per lane; slot s belongs to the
-                // term whose range holds it (the last head at or before s)
-                for (uint32_t wb = 0; wb < total; wb += kWarp) {
-                    uint32_t hb = 0;
-                    if (cnt > 0 && excl < wb + kWarp && excl + cnt > wb) {
-                        const uint32_t pos = excl > wb ? excl - wb : 0u;
-                        hb = 1u << pos;
-                        sm_st_u8(s_tat + pos, static_cast<uint32_t>(lane));
-                    }
-                    const uint32_t heads = __reduce_or_sync(0xFFFFFFFFu, hb);
-                    __syncwarp();
-                    const uint32_t sl = wb + lane;
-                    if (sl < total) {
-                        const int ph = 31 - __clz(heads & lane_le);
-                        const uint2 en = sm_ld_u64(s_ts + 8u * sm_ld_u8(s_tat + ph));
-                        const uint2 pr = ld_pair(pairs + (en.x + sl), pol_keep);
-                        if (pr.x != own_l) {
-                            const int qv = __float2int_rn(__uint_as_float(en.y) * __uint_as_float(pr.y) * kFixScale);
+                    for (int q = 0; q < 4; ++q)
+                        pr[q] = k0 + q < cnt ? ld_pair(pairs + ext.x + k0 + q, pol_keep) : make_uint2(kNone, 0u);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (pr[q].x != kNone && pr[q].x != own_l) {
+                            const int qv = __float2int_rn(xs * __uint_as_float(pr[q].y));
                             if (qv != 0) {
-                                const int old = sm_atom_add(s_acc + 4u * pr.x, qv);
+                                const int old = sm_atom_add(s_acc + 4u * pr[q].x, qv);
                                 if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
                                     const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
-                                    if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr.x);
+                                    if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr[q].x);
                                 }
                             }
                         }
                     }
-                    __syncwarp();
                 }
+                __syncwarp();
                 if (need_dot)  // own dot, ascending entry order, exact in fp64
                     s_own = fold_chunk(s_own, static_cast<double>(x) * static_cast<double>(cv),
                                        static_cast<int>(imin64(kWarp, end - e0)), lane, fold);
@@ -421,8 +403,10 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         atomicAdd(p.n_cand_nnz, static_cast<unsigned long long>(cnnz));
         atomicAdd(p.n_visits, static_cast<unsigned long long>(visits));
         atomicAdd(p.n_own, static_cast<unsigned long long>(owns));
-        atomicAdd(p.n_pairs, static_cast<unsigned long long>(npairs));
-    }
+        }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) npairs += __shfl_xor_sync(0xFFFFFFFFu, npairs, off);  // per-lane terms
+    if (lane == 0) atomicAdd(p.n_pairs, static_cast<unsigned long long>(npairs));
 }
 
 // High postings of the cluster tile [c0, c0 + kt) of M in one pass over M:
