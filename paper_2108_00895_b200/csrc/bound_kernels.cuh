@@ -125,6 +125,25 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// Loads and a conversion as volatile asm: the compiler keeps them where they
+// are written (it otherwise converts a gathered weight right after its load,
+// stalling the warp on it before the next chunk's loads are issued).
+__device__ __forceinline__ uint2 ld_u2_nc(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_f32_nc(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double cvt_f64(float v) {
+    double r;
+    asm volatile("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(v));
+    return r;
+}
+
 // Fold the lanes' exact fp64 products of one chunk into s in ascending entry
 // order (every lane folds the same sequence: s is warp-uniform).
 __device__ __forceinline__ double fold_chunk(double s, double prod, int n, int lane, double* wsm) {
@@ -269,14 +288,8 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 const bool valid = e0 + lane < end;
                 const int32_t t = t_n;
                 const float x = x_n;
-                // this chunk's postings extent and own-column weight
-                uint2 ext = make_uint2(0u, 0u);
-                float cv = 0.f;
-                if (valid) {
-                    ext = __ldg(p.hptr + t);
-                    if (need_dot) cv = __ldg(p.CT + static_cast<uint64_t>(t) * p.ld_ct + arg);
-                }
-                // the next chunk: this document's, else the next document's first
+                // the next chunk first (this document's, else the next document's),
+                // so its loads fly while this chunk waits on its own
                 {
                     const bool last = e0 + kWarp >= end;
                     const int64_t en = last ? beg_n + lane : e0 + kWarp + lane;
@@ -288,6 +301,14 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                         x_n = ld_stream_f32(p.val + en, pol_stream);
                     }
                     if (last) pref_done = true;
+                }
+                // this chunk's postings extent and own-column weight (the weight
+                // is first used by the fold, after the pairs)
+                uint2 ext = make_uint2(0u, 0u);
+                float cv = 0.f;
+                if (valid) {
+                    ext = ld_u2_nc(p.hptr + t);
+                    if (need_dot) cv = ld_f32_nc(p.CT + static_cast<uint64_t>(t) * p.ld_ct + arg);
                 }
                 // the term's high pairs, up to 4 per round with their loads in
                 // flight together (lists average ~1 pair on the TF-IDF corpora);
@@ -316,7 +337,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 }
                 __syncwarp();
                 if (need_dot)  // own dot, ascending entry order, exact in fp64
-                    s_own = fold_chunk(s_own, static_cast<double>(x) * static_cast<double>(cv),
+                    s_own = fold_chunk(s_own, cvt_f64(x) * cvt_f64(cv),
                                        static_cast<int>(imin64(kWarp, end - e0)), lane, fold);
             }
         }

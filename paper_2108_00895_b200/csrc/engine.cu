@@ -1228,8 +1228,9 @@ private:
         btake_.alloc(n_);
         bctr_.alloc(8);
         CK(cudaMemsetAsync(bctr_.p, 0, 8 * sizeof(unsigned long long), stream_));
-        const float thr = theta_;
+        const float thr = theta_adapt_ ? tctl_[init].theta : theta_;
         const uint32_t KT = ncols <= 1024 ? 1024 : 2048;
+        double pass_ms = 0.0;
         BoundArgs p{};
         p.indptr = indptr_.p;
         p.idx = idx_.p;
@@ -1286,6 +1287,7 @@ private:
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
             screen_ms_ += ms;
+            pass_ms += ms;
             screen_launches_ += 1;
         }
         if (init == kInitNcc)
@@ -1315,14 +1317,24 @@ private:
                          static_cast<unsigned long long>(n_fb), static_cast<unsigned long long>(ctr[0]),
                          static_cast<unsigned long long>(ctr[1]), static_cast<unsigned long long>(ctr[3]),
                          p.same != nullptr);
+        // θ for the next pass of this kind: hill-climb the measured screen time
+        // per work item (θ trades high pairs against candidate dots, and the
+        // balance differs per corpus); back off when documents fall through to
+        // the exact scan. θ never changes a result.
         if (theta_adapt_ && n_work > 0) {
+            ThetaCtl& c = tctl_[init];
             const double fb = static_cast<double>(n_fb) / static_cast<double>(n_work);
-            const double cpd = n_list ? static_cast<double>(ctr[0]) / static_cast<double>(n_list) : 0.0;
-            if (fb > 2e-3 || cpd > 2.0)
-                theta_ *= 0.7f;
-            else if (cpd < 0.3)
-                theta_ *= 1.25f;
-            theta_ = std::min(0.25f, std::max(1e-5f, theta_));
+            const double cost = pass_ms / static_cast<double>(n_work);
+            if (fb > 2e-3) {
+                c.theta *= 0.7f;
+                c.dir = -1;
+                c.last = -1.0;
+            } else {
+                if (c.last > 0.0 && cost > c.last * 1.02) c.dir = -c.dir;
+                c.last = cost;
+                c.theta *= c.dir > 0 ? 1.25f : 0.8f;
+            }
+            c.theta = std::min(0.25f, std::max(1e-5f, c.theta));
         }
     }
 
@@ -1742,7 +1754,13 @@ private:
     bool bound_enabled_ = true;   // bound screen (SSKM_BOUND=0: the full postings / dense screens)
     bool theta_adapt_ = true;
     bool debug_ = false;  // SSKM_DEBUG=1: per-assign screen counters on stderr
-    float theta_ = 0.004f;        // high/low split of the centroid weights (SSKM_THETA)
+    float theta_ = 0.004f;        // fixed high/low split of the centroid weights (SSKM_THETA)
+    struct ThetaCtl {
+        float theta = 0.004f;  // adaptive split, per pass kind (full, NCC pass A, rescan)
+        int dir = 1;
+        double last = -1.0;    // screen ms per work item at the previous step
+    };
+    ThetaCtl tctl_[3];
     // per-assign bound-screen totals (stats)
     uint64_t bstat_docs_ = 0, bstat_pairs_ = 0, bstat_cand_ = 0, bstat_doc_nnz_ = 0, bstat_cand_nnz_ = 0,
              bstat_visits_ = 0, bstat_own_ = 0;

@@ -17,6 +17,8 @@ for it in range(1, iters + 1):
                           assign_ms=round(st.assign_ms, 2), screen_ms=round(st.screen_ms, 2), tiles=st.screen_launches,
                           n_changed=st.n_changed, density=round(st.centroid_density, 4), n_reassigned=st.n_reassigned, n_exact=st.n_exact,
                           n_rescan=st.n_rescan, n_repaired=st.n_repaired, dots=st.dot_products,
+                          bound=dict(theta=round(st.bound_theta, 5), pairs=st.bound_pairs, cands=st.bound_candidates,
+                                     own=st.bound_own_dots, docs=st.bound_docs),
                           **({} if not st.index_active else dict(idx_build_ms=round(st.index_build_seconds * 1e3, 2), idx_queries=st.index_queries, idx_cands=st.candidates_total)))), flush=True)
 if os.environ.get("PROBE_PAIRS"):
     pairs = eng.postings_work()
