@@ -41,6 +41,7 @@ constexpr double kFixUnit = 0x1p-30;
 
 struct BoundArgs {
     const int64_t* indptr;
+    const uint32_t* indptr32;  // 32-bit copy of indptr (nnz < 2^32 per device)
     const int32_t* idx;
     const float* val;
     const uint2* hptr;         // high postings of the tile: (first pair, count) per term
@@ -81,7 +82,8 @@ struct BoundSmem {
     static constexpr uint32_t o_fold = o_acc + KT * 4;     // double[32] fold buffer
     static constexpr uint32_t o_tl = o_fold + 32 * 8;      // u16[kCap] touched list
     static constexpr uint32_t o_cnt = o_tl + kCap * 2;     // u32 touched count
-    static constexpr size_t per_warp = o_cnt + 16;
+    static constexpr uint32_t o_stats = o_cnt + 16;        // u32[8] per-warp statistics
+    static constexpr size_t per_warp = o_stats + 32;
 };
 
 __device__ __forceinline__ uint32_t sm_ld_u32(uint32_t a) {
@@ -196,10 +198,12 @@ __device__ __forceinline__ double gamma_ub(double n, double u) {
 // the next document's extents and start cluster one document ahead (its id two
 // ahead) and every chunk's (term, weight) one chunk ahead, across document
 // boundaries; per chunk, the terms' high-postings extents and own-column
-// weights are gathered together, then the chunk's high pairs are taken in
-// windows of 32 slots (one pair per lane) into the fixed-point accumulators
-// with shared integer atomics; the first touch of a cluster appends it to the
-// touched list.
+// weights are gathered together, then each lane takes its term's high pairs,
+// up to 4 loads in flight, into the fixed-point accumulators with shared
+// integer atomics; the first touch of a cluster appends it to the touched list.
+// Offsets are 32-bit (the host requires nnz < 2^32 per device for this kernel)
+// and the statistics counters live in shared memory, to keep the pipelined
+// loads in registers.
 template <int KT, int INIT>
 __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(BoundArgs p) {
     using SM = BoundSmem<KT>;
@@ -210,28 +214,32 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     unsigned char* base = smem_b + static_cast<size_t>(warp) * SM::per_warp;
     const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(base));
     double* fold = reinterpret_cast<double*>(base + SM::o_fold);
-    const uint32_t s_acc = sb + SM::o_acc, s_tl = sb + SM::o_tl, s_cnt = sb + SM::o_cnt;
+    const uint32_t s_acc = sb + SM::o_acc, s_tl = sb + SM::o_tl, s_cnt = sb + SM::o_cnt, s_st = sb + SM::o_stats;
     for (int c = lane; c < KT; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
+    if (lane < 8) sm_st_u32(s_st + 4u * lane, 0u);
     __syncwarp();
     const uint2* __restrict__ pairs = p.pairs;
     const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-    const int64_t chunk = static_cast<int64_t>(ceil_div(p.n_work, gridDim.x));
-    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * chunk;
-    const int64_t w1 = imin64(p.n_work, w0 + chunk);
+    const uint32_t n_work = static_cast<uint32_t>(p.n_work);
+    const uint32_t chunk = static_cast<uint32_t>(ceil_div(n_work, gridDim.x));
+    const uint32_t w0 = blockIdx.x * chunk;
+    const uint32_t w1 = min(n_work, w0 + chunk);
     const bool first = p.first != 0;
-    uint32_t cands = 0, npairs = 0, dnnz = 0, cnnz = 0, visits = 0, owns = 0;
-    auto doc_of = [&](int64_t ww) -> uint32_t { return p.order ? __ldg(p.order + ww) : static_cast<uint32_t>(ww); };
+    const uint32_t* __restrict__ indptr = reinterpret_cast<const uint32_t*>(p.indptr32);
+    auto doc_of = [&](uint32_t ww) -> uint32_t { return p.order ? __ldg(p.order + ww) : ww; };
     auto start_of = [&](uint32_t i) -> uint32_t {
         if constexpr (INIT == kInitNcc) return first ? __ldg(p.a_start + i) : p.a[i];
         return p.a[i];
     };
-    int64_t w = w0 + warp;
-    uint32_t i_n = 0, i_nn = 0, arg_n = 0;
-    int64_t beg_n = 0, end_n = 0;
+    auto stat = [&](int k, uint32_t v) {  // per-warp statistics (lane 0)
+        if (lane == 0) sm_st_u32(s_st + 4u * k, sm_ld_u32(s_st + 4u * k) + v);
+    };
+    uint32_t w = w0 + warp;
+    uint32_t i_n = 0, i_nn = 0, arg_n = 0, beg_n = 0, end_n = 0;
     if (w < w1) {
         i_n = doc_of(w);
-        beg_n = __ldg(p.indptr + i_n);
-        end_n = __ldg(p.indptr + i_n + 1);
+        beg_n = __ldg(indptr + i_n);
+        end_n = __ldg(indptr + i_n + 1);
         arg_n = start_of(i_n);
     }
     if (w + nwarps < w1) i_nn = doc_of(w + nwarps);
@@ -242,14 +250,13 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         x_n = ld_stream_f32(p.val + beg_n + lane, pol_stream);
     }
     for (; w < w1; w += nwarps) {
-        const uint32_t i = i_n;
-        const int64_t beg = beg_n, end = end_n;
+        const uint32_t i = i_n, beg = beg_n, end = end_n;
         uint32_t arg = arg_n;
-        const int64_t wn = w + nwarps;
+        const uint32_t wn = w + nwarps;
         if (wn < w1) {
             i_n = i_nn;
-            beg_n = __ldg(p.indptr + i_n);
-            end_n = __ldg(p.indptr + i_n + 1);
+            beg_n = __ldg(indptr + i_n);
+            end_n = __ldg(indptr + i_n + 1);
             arg_n = start_of(i_n);
         }
         if (wn + nwarps < w1) i_nn = doc_of(wn + nwarps);
@@ -282,9 +289,9 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         double s_own = 0.0;
         bool pref_done = false;
         if (active) {
-            ++visits;
-            dnnz += static_cast<uint32_t>(end - beg);
-            for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
+            stat(0, 1u);
+            stat(1, end - beg);
+            for (uint32_t e0 = beg; e0 < end; e0 += kWarp) {
                 const bool valid = e0 + lane < end;
                 const int32_t t = t_n;
                 const float x = x_n;
@@ -292,8 +299,8 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 // so its loads fly while this chunk waits on its own
                 {
                     const bool last = e0 + kWarp >= end;
-                    const int64_t en = last ? beg_n + lane : e0 + kWarp + lane;
-                    const int64_t lim = last ? (wn < w1 ? end_n : 0) : end;
+                    const uint32_t en = last ? beg_n + lane : e0 + kWarp + lane;
+                    const uint32_t lim = last ? (wn < w1 ? end_n : 0u) : end;
                     t_n = 0;
                     x_n = 0.f;
                     if (en < lim) {
@@ -314,7 +321,6 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 // flight together (lists average ~1 pair on the TF-IDF corpora);
                 // longer lists loop on in the lanes that have them
                 const uint32_t cnt = ext.y;
-                npairs += cnt;
                 const float xs = x * kFixScale;
                 for (uint32_t k0 = 0; k0 < cnt; k0 += 4) {
                     uint2 pr[4];
@@ -336,9 +342,10 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     }
                 }
                 __syncwarp();
+                stat(2, __reduce_add_sync(0xFFFFFFFFu, cnt));
                 if (need_dot)  // own dot, ascending entry order, exact in fp64
-                    s_own = fold_chunk(s_own, cvt_f64(x) * cvt_f64(cv),
-                                       static_cast<int>(imin64(kWarp, end - e0)), lane, fold);
+                    s_own = fold_chunk(s_own, cvt_f64(x) * cvt_f64(cv), static_cast<int>(min(32u, end - e0)), lane,
+                                       fold);
             }
         }
         if (!pref_done) {  // empty or skipped document: prefetch the next one's first chunk
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         if (first && active) {
             if (need_dot) {
                 best = s_own;
-                ++owns;
+                stat(3, 1u);
             }
             // no cluster without a high entry shared with x can exceed lb
             const double lb = p.theta * xb.x * (1.0 + 1e-12) + g64 * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
@@ -395,8 +402,8 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     const double u = __shfl_sync(0xFFFFFFFFu, ub, src);
                     if (u >= best) {  // best only grows: re-check
                         const double s = cand_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, g, lane, fold);
-                        ++cands;
-                        cnnz += static_cast<uint32_t>(end - beg);
+                        stat(4, 1u);
+                        stat(5, end - beg);
                         if (s > best || (s == best && g < arg)) {
                             best = s;
                             arg = g;
@@ -419,15 +426,13 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         __syncwarp();
     }
     if (lane == 0) {
-        atomicAdd(p.n_cand, static_cast<unsigned long long>(cands));
-        atomicAdd(p.n_doc_nnz, static_cast<unsigned long long>(dnnz));
-        atomicAdd(p.n_cand_nnz, static_cast<unsigned long long>(cnnz));
-        atomicAdd(p.n_visits, static_cast<unsigned long long>(visits));
-        atomicAdd(p.n_own, static_cast<unsigned long long>(owns));
-        }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) npairs += __shfl_xor_sync(0xFFFFFFFFu, npairs, off);  // per-lane terms
-    if (lane == 0) atomicAdd(p.n_pairs, static_cast<unsigned long long>(npairs));
+        atomicAdd(p.n_visits, static_cast<unsigned long long>(sm_ld_u32(s_st + 0)));
+        atomicAdd(p.n_doc_nnz, static_cast<unsigned long long>(sm_ld_u32(s_st + 4)));
+        atomicAdd(p.n_pairs, static_cast<unsigned long long>(sm_ld_u32(s_st + 8)));
+        atomicAdd(p.n_own, static_cast<unsigned long long>(sm_ld_u32(s_st + 12)));
+        atomicAdd(p.n_cand, static_cast<unsigned long long>(sm_ld_u32(s_st + 16)));
+        atomicAdd(p.n_cand_nnz, static_cast<unsigned long long>(sm_ld_u32(s_st + 20)));
+    }
 }
 
 // High postings of the cluster tile [c0, c0 + kt) of M in one pass over M:
@@ -498,6 +503,12 @@ __global__ void bound_ncc_rescan_kernel(const uint32_t* __restrict__ order, int6
             rescan_list[pos] = i;
         }
     }
+}
+
+__global__ void narrow_u32_kernel(const int64_t* __restrict__ in, int64_t n, uint32_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<uint32_t>(in[i]);
 }
 
 // Per-document bound inputs, once per upload: (‖x‖₁, ‖x‖₂) rounded up to fp32

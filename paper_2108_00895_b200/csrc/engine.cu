@@ -184,6 +184,14 @@ public:
         xb_.alloc(n);
         launch(doc_bound_norms_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p, xb_.p);
         CK_LAUNCH();
+        // the bound screen's 32-bit offsets (its registers hold a pipeline of
+        // them); above 2^32 nonzeros per device the postings screens are used
+        bound_ok_ = nnz_ < (int64_t(1) << 32);
+        if (bound_ok_) {
+            indptr32_.alloc(n + 1);
+            launch(narrow_u32_kernel, grid_for(n + 1, 256), 256, indptr_.p, n + 1, indptr32_.p);
+            CK_LAUNCH();
+        }
         // fixed-point scale: N_total · 2^K <= 2^62 with |x| <= 1
         int lg = 0;
         while ((int64_t(1) << lg) < n_total_) ++lg;
@@ -241,6 +249,7 @@ public:
         chg_ids_.alloc(k_);
         drift_.alloc(k_);
         norm2_.alloc(k_);
+        Q_.alloc(2 * static_cast<size_t>(k_));
         drift_rec_.alloc(k_);
         part_.alloc(ceil_div(d_, kRowBlock) * k_);
         state_ = false;
@@ -254,6 +263,7 @@ public:
     // -------------------------------------------------------------- init --
     void reset_sums() {
         CK(cudaMemsetAsync(S_.p, 0, static_cast<uint64_t>(d_) * ld_ * sizeof(long long), stream_));
+        CK(cudaMemsetAsync(Q_.p, 0, 2 * static_cast<size_t>(k_) * sizeof(unsigned long long), stream_));
         launch(fill_u32_kernel, grid_for(n_, 256), 256, a_sum_.p, n_, kNone);
         CK_LAUNCH();
         CK(cudaMemsetAsync(touched_.p, 0, k_, stream_));
@@ -376,7 +386,7 @@ public:
         CK_LAUNCH();
         launch(delta_local_kernel, grid_for(n_ * 32, 256), 256, 
             indptr_.p, idx_.p, val_.p, moved_.p, &scal_.p->n_moved, a_.p, a_sum_.p, S_.p, ld_, K_,
-            touched_.p);
+            touched_.p, Q_.p);
         CK_LAUNCH();
         finish_update(st);
         CK(cudaEventRecord(ev_[1], stream_));
@@ -405,7 +415,7 @@ public:
         reset_scalars();
         if (n_moved > 0) {
             launch(delta_packed_kernel, grid_for(n_moved * 32, 256), 256, 
-                n_moved, old_c, new_c, row_ptr, idx, val, S_.p, ld_, K_, touched_.p);
+                n_moved, old_c, new_c, row_ptr, idx, val, S_.p, ld_, K_, touched_.p, Q_.p);
             CK_LAUNCH();
         }
         finish_update(st);
@@ -1096,9 +1106,8 @@ private:
         const uint32_t n_rb = static_cast<uint32_t>(ceil_div(d_, kRowBlock));
         if (n_rec > 0) {
             dim3 grid(static_cast<unsigned>(ceil_div(n_rec, 128)), n_rb);
-            launch(norm2_partial_kernel, grid, 128, S_.p, ld_, d_, rec_ids_.p, n_rec, part_.p);
-            launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(n_rec, 128)), 128, 
-                part_.p, n_rb, n_rec, norm2_.p);
+            launch(q_norm2_kernel, static_cast<unsigned>(ceil_div(n_rec, 128)), 128, Q_.p, rec_ids_.p, n_rec,
+                   norm2_.p);
             launch(write_cols_kernel, grid, 128, S_.p, ct_.p, ld_, d_, rec_ids_.p, n_rec, norm2_.p,
                                                          part_.p, &scal_.p->zero_flag);
             launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(n_rec, 128)), 128, 
@@ -1233,6 +1242,7 @@ private:
         double pass_ms = 0.0;
         BoundArgs p{};
         p.indptr = indptr_.p;
+        p.indptr32 = indptr32_.p;
         p.idx = idx_.p;
         p.val = val_.p;
         p.col_ids = col_ids;
@@ -1388,7 +1398,7 @@ private:
                     const uint32_t* order, int64_t n_work, int init) {
         // the bound screen needs a real assignment to start from: not the
         // seed assignment (iteration 0), whose state is all cluster 0
-        if (bound_enabled_ && iteration_ >= 1) {
+        if (bound_enabled_ && bound_ok_ && iteration_ >= 1) {
             bound_assign(M, ld, ncols, col_ids, order, n_work, init);
             return true;  // candidates resolved exactly in the kernel; the exact list holds the rest
         }
@@ -1721,6 +1731,8 @@ private:
     DevBuf<int32_t> idx_;
     DevBuf<float> val_;
     DevBuf<float2> xb_;
+    DevBuf<uint32_t> indptr32_;
+    bool bound_ok_ = false;  // nnz < 2^32 on this device
     DevBuf<uint8_t> btake_, same_;
     DevBuf<uint32_t> bcol_of_;
     DevBuf<uint2> hptr_;
@@ -1774,6 +1786,7 @@ private:
     DevBuf<uint32_t> sa_, exact_;
     DevBuf<uint32_t> order_, keys32_;
     DevBuf<double> sims_, drift_, norm2_, drift_rec_, part_, obj_part_;
+    DevBuf<unsigned long long> Q_;  // exact Σ_t S[t][j]² per column (128-bit: lo, hi)
     DevBuf<uint8_t> unchanged_, touched_, repaired_flag_;
     DevBuf<unsigned long long> counts_, keys_;
     DevBuf<uint32_t> vals_, moves_, mv_old_, mv_new_;

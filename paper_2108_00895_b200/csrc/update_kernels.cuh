@@ -12,6 +12,12 @@
 // renormalised (fp64) and rewritten; a cluster with unchanged membership keeps
 // a bitwise-identical column, which is exactly the reference's ncc_epsilon = 0
 // "unchanged" condition.
+//
+// The squared column norms Q_j = Σ_t S[t][j]² are kept alongside as exact
+// 128-bit integers (|S| ≤ 2^62 per column norm, so Q_j < 2^124): every atomic
+// S += q returns the old value s, and Q_j += q·(2s + q) telescopes to the new
+// Q_j whatever the order of the atomics. A renormalisation therefore reads
+// only the columns it rewrites, once.
 #pragma once
 
 #include "common.cuh"
@@ -54,13 +60,41 @@ __device__ __forceinline__ long long quantize(float x, int K) {
     return __double2ll_rn(ldexp(static_cast<double>(x), K));
 }
 
+// S[row + c] += q; returns q·(2·old + q), the exact change of Σ S² (128-bit).
+__device__ __forceinline__ __int128 add_sum(long long* S, uint64_t o, long long q) {
+    const long long old = static_cast<long long>(
+        atomicAdd(reinterpret_cast<unsigned long long*>(S + o), static_cast<unsigned long long>(q)));
+    return static_cast<__int128>(q) * (2 * static_cast<__int128>(old) + q);
+}
+
+__device__ __forceinline__ __int128 warp_sum128(__int128 v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long lo = __shfl_xor_sync(0xFFFFFFFFu, static_cast<unsigned long long>(v), off);
+        const long long hi = __shfl_xor_sync(0xFFFFFFFFu, static_cast<long long>(v >> 64), off);
+        v += (static_cast<__int128>(hi) << 64) | static_cast<__int128>(lo);
+    }
+    return v;
+}
+
+// Q (lo, hi words) += v modulo 2^128: the low word's carry, seen in the value
+// its atomic returns, goes into the high word's atomic. The final pair is exact
+// in any interleaving.
+__device__ __forceinline__ void atomic_add128(unsigned long long* q, __int128 v) {
+    const unsigned long long lo = static_cast<unsigned long long>(v);
+    const unsigned long long hi = static_cast<unsigned long long>(v >> 64);
+    const unsigned long long old = atomicAdd(q, lo);
+    atomicAdd(q + 1, hi + (old + lo < old ? 1ull : 0ull));
+}
+
 // Apply the rows of locally moved documents: warp per document, lanes over its
 // nonzeros (distinct terms, so no intra-row conflicts); integer atomics only.
 __global__ void delta_local_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
                                    const float* __restrict__ val, const uint32_t* __restrict__ moved,
                                    const unsigned long long* n_moved_p, const uint32_t* __restrict__ a,
                                    uint32_t* __restrict__ a_sum, long long* __restrict__ S,
-                                   uint64_t ld, int K, uint8_t* __restrict__ touched) {
+                                   uint64_t ld, int K, uint8_t* __restrict__ touched,
+                                   unsigned long long* __restrict__ Q) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
@@ -69,50 +103,66 @@ __global__ void delta_local_kernel(const int64_t* __restrict__ indptr, const int
         const uint32_t i = moved[m];
         const uint32_t nc = a[i], oc = a_sum[i];
         const int64_t beg = indptr[i], end = indptr[i + 1];
+        __int128 dn = 0, dold = 0;
         for (int64_t e = beg + lane; e < end; e += kWarp) {
             const long long q = quantize(val[e], K);
             const uint64_t row = static_cast<uint64_t>(idx[e]) * ld;
-            atomicAdd(reinterpret_cast<unsigned long long*>(S + row + nc),
-                      static_cast<unsigned long long>(q));
-            if (oc != kNone)
-                atomicAdd(reinterpret_cast<unsigned long long*>(S + row + oc),
-                          static_cast<unsigned long long>(-q));
+            dn += add_sum(S, row + nc, q);
+            if (oc != kNone) dold += add_sum(S, row + oc, -q);
         }
-        __syncwarp();
+        dn = warp_sum128(dn);
+        if (oc != kNone) dold = warp_sum128(dold);
         if (lane == 0) {
+            atomic_add128(Q + 2ull * nc, dn);
             touched[nc] = 1;
-            if (oc != kNone) touched[oc] = 1;
+            if (oc != kNone) {
+                atomic_add128(Q + 2ull * oc, dold);
+                touched[oc] = 1;
+            }
             a_sum[i] = nc;
         }
     }
 }
 
-// Same for rows gathered from all ranks (multi-GPU delta exchange): packed
-// (old, new, row_ptr, idx, val) records, any order.
+// Multi-GPU: apply the packed rows gathered from every rank (delta exchange).
 __global__ void delta_packed_kernel(int64_t n_moved, const uint32_t* __restrict__ old_c,
                                     const uint32_t* __restrict__ new_c,
                                     const int64_t* __restrict__ row_ptr,
                                     const int32_t* __restrict__ idx, const float* __restrict__ val,
                                     long long* __restrict__ S, uint64_t ld, int K,
-                                    uint8_t* __restrict__ touched) {
+                                    uint8_t* __restrict__ touched, unsigned long long* __restrict__ Q) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
     for (uint64_t m = gw; m < static_cast<uint64_t>(n_moved); m += nw) {
         const uint32_t nc = new_c[m], oc = old_c[m];
+        __int128 dn = 0, dold = 0;
         for (int64_t e = row_ptr[m] + lane; e < row_ptr[m + 1]; e += kWarp) {
             const long long q = quantize(val[e], K);
             const uint64_t row = static_cast<uint64_t>(idx[e]) * ld;
-            atomicAdd(reinterpret_cast<unsigned long long*>(S + row + nc),
-                      static_cast<unsigned long long>(q));
-            if (oc != kNone)
-                atomicAdd(reinterpret_cast<unsigned long long*>(S + row + oc),
-                          static_cast<unsigned long long>(-q));
+            dn += add_sum(S, row + nc, q);
+            if (oc != kNone) dold += add_sum(S, row + oc, -q);
         }
+        dn = warp_sum128(dn);
+        if (oc != kNone) dold = warp_sum128(dold);
         if (lane == 0) {
+            atomic_add128(Q + 2ull * nc, dn);
             touched[nc] = 1;
-            if (oc != kNone) touched[oc] = 1;
+            if (oc != kNone) {
+                atomic_add128(Q + 2ull * oc, dold);
+                touched[oc] = 1;
+            }
         }
+    }
+}
+
+// ‖S_j‖² of the recomputed columns from the exact 128-bit Q_j (< 2^124, ≥ 0).
+__global__ void q_norm2_kernel(const unsigned long long* __restrict__ Q, const uint32_t* __restrict__ ids,
+                               uint32_t n_ids, double* __restrict__ norm2) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_ids; c += gridDim.x * blockDim.x) {
+        const uint32_t j = ids[c];
+        const unsigned long long lo = Q[2ull * j], hi = Q[2ull * j + 1];
+        norm2[c] = static_cast<double>(hi) * 0x1p64 + static_cast<double>(lo);
     }
 }
 
@@ -195,23 +245,6 @@ __global__ void compact_ids_kernel(const uint8_t* __restrict__ flags, uint32_t k
 }
 
 constexpr int kRowBlock = 512;  // rows per partial in the column reductions
-
-// Σ_t S[t][j]² per recomputed column j, as fixed-order partials over row blocks.
-__global__ void norm2_partial_kernel(const long long* __restrict__ S, uint64_t ld, uint32_t d,
-                                     const uint32_t* __restrict__ ids, uint32_t n_ids,
-                                     double* __restrict__ part) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t rb = blockIdx.y;
-    if (c >= n_ids) return;
-    const uint32_t j = ids[c];
-    const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
-    double s = 0.0;
-    for (uint32_t t = t0; t < t1; ++t) {
-        const double v = static_cast<double>(S[static_cast<uint64_t>(t) * ld + j]);
-        s = fma(v, v, s);
-    }
-    part[static_cast<uint64_t>(rb) * n_ids + c] = s;
-}
 
 __global__ void reduce_partials_kernel(const double* __restrict__ part, uint32_t n_rb,
                                        uint32_t n_ids, double* __restrict__ out) {
