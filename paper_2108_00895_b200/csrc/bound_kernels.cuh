@@ -44,7 +44,7 @@ struct BoundArgs {
     const uint32_t* indptr32;  // 32-bit copy of indptr (nnz < 2^32 per device)
     const int32_t* idx;
     const float* val;
-    const uint2* hptr;         // high postings of the tile: (first pair, count) per term
+    const uint4* hptr;         // per term: (first high pair, count, bits of the largest low |weight|, 0)
     const uint2* pairs;        // (column in tile, value bits)
     uint32_t c0, kt;
     const uint32_t* col_ids;   // column -> cluster id (nullptr = identity)
@@ -57,6 +57,7 @@ struct BoundArgs {
     double theta, cmax;
     uint32_t k;
     int first;                 // first tile: establish the baseline and decide take
+    int single_tile;           // the tile holds every column (its low maxima bound every cluster)
     uint32_t* a;               // in/out: running exact argmax
     double* sims;              // in/out: running exact max
     const uint8_t* unchanged;  // NCC: cached own similarity valid
@@ -130,9 +131,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Loads and a conversion as volatile asm: the compiler keeps them where they
 // are written (it otherwise converts a gathered weight right after its load,
 // stalling the warp on it before the next chunk's loads are issued).
-__device__ __forceinline__ uint2 ld_u2_nc(const uint2* p) {
-    uint2 v;
-    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+__device__ __forceinline__ uint4 ld_u4_nc(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
 __device__ __forceinline__ float ld_f32_nc(const float* p) {
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         if (lane == 0) sm_st_u32(s_cnt, 0u);
         __syncwarp();
         double s_own = 0.0;
+        float lowsum = 0.f;  // Σ |x_t|·(largest low |weight| of term t): bounds every cluster's low part
         bool pref_done = false;
         if (active) {
             stat(0, 1u);
@@ -311,10 +313,10 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 }
                 // this chunk's postings extent and own-column weight (the weight
                 // is first used by the fold, after the pairs)
-                uint2 ext = make_uint2(0u, 0u);
+                uint4 ext = make_uint4(0u, 0u, 0u, 0u);
                 float cv = 0.f;
                 if (valid) {
-                    ext = ld_u2_nc(p.hptr + t);
+                    ext = ld_u4_nc(p.hptr + t);
                     if (need_dot) cv = ld_f32_nc(p.CT + static_cast<uint64_t>(t) * p.ld_ct + arg);
                 }
                 // the term's high pairs, up to 4 per round with their loads in
@@ -322,6 +324,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 // longer lists loop on in the lanes that have them
                 const uint32_t cnt = ext.y;
                 const float xs = x * kFixScale;
+                lowsum = fmaf(fabsf(x), __uint_as_float(ext.z), lowsum);
                 for (uint32_t k0 = 0; k0 < cnt; k0 += 4) {
                     uint2 pr[4];
 #pragma unroll
@@ -361,13 +364,20 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         const double nn = static_cast<double>(end - beg);
         const double g32 = gamma_ub(nn + 32.0, 0x1p-24), g64 = gamma_ub(nn, 0x1p-53);
         const double tiny = nn * kFixUnit + nn * 0x1p-126;
+        // the lanes' fp32 sums of nonnegative terms, each within (1 + (n/32 + 1)·2^-24)
+        double low = static_cast<double>(lowsum);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) low += __shfl_xor_sync(0xFFFFFFFFu, low, off);
+        low = low * (1.0 + (nn / 32.0 + 2.0) * 0x1p-23) * (1.0 + 1e-12);
+        const double theta_x1 = p.theta * xb.x * (1.0 + 1e-12);
         if (first && active) {
             if (need_dot) {
                 best = s_own;
                 stat(3, 1u);
             }
             // no cluster without a high entry shared with x can exceed lb
-            const double lb = p.theta * xb.x * (1.0 + 1e-12) + g64 * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
+            // (the tile's low maxima bound the clusters of this tile only)
+            const double lb = (p.single_tile ? fmin(low, theta_x1) : theta_x1) + g64 * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
             const bool take = best > lb && (INIT != kInitFull || arg < p.k);
             if (lane == 0) {
                 p.take[w] = take ? 1 : 0;
@@ -380,9 +390,44 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         }
         const bool dense = ntouch > static_cast<uint32_t>(kCap);
         if (active) {
-            // candidates: touched clusters whose upper bound reaches the running best
-            const double bx = p.theta * xb.x * (1.0 + 1e-12) + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
+            // candidates: touched clusters whose upper bound reaches the running
+            // best, gathered 32 at a time (one per lane) and evaluated in
+            // descending bound order, so the likely winner raises `best` first
+            // and prunes the rest (a bound below best cannot win or tie)
+            const double bx = fmin(low, theta_x1) + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
             const uint32_t count = dense ? p.kt : ntouch;
+            uint32_t c_gid = 0;   // this lane's pending candidate
+            double c_ub = -1e300;
+            bool c_on = false;
+            auto drain = [&](bool all) {
+                // evaluate pending candidates, best bound first; with !all only
+                // until a lane is free again
+                while (true) {
+                    c_on = c_on && c_ub >= best;
+                    const unsigned on = __ballot_sync(0xFFFFFFFFu, c_on);
+                    if (!on || (!all && on != 0xFFFFFFFFu)) break;
+                    double mu = c_on ? c_ub : -1e300;
+                    int ml = lane;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const double ou = __shfl_xor_sync(0xFFFFFFFFu, mu, off);
+                        const int ol = __shfl_xor_sync(0xFFFFFFFFu, ml, off);
+                        if (ou > mu || (ou == mu && ol < ml)) {
+                            mu = ou;
+                            ml = ol;
+                        }
+                    }
+                    const uint32_t g = __shfl_sync(0xFFFFFFFFu, c_gid, ml);
+                    if (lane == ml) c_on = false;
+                    const double sx = cand_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, g, lane, fold);
+                    stat(4, 1u);
+                    stat(5, end - beg);
+                    if (sx > best || (sx == best && g < arg)) {
+                        best = sx;
+                        arg = g;
+                    }
+                }
+            };
             for (uint32_t k0 = 0; k0 < count; k0 += kWarp) {
                 const uint32_t kk = k0 + lane;
                 bool cand = false;
@@ -395,22 +440,33 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     cand = gid != arg && ub >= best;
                 }
                 unsigned cm = __ballot_sync(0xFFFFFFFFu, cand);
+                // place the new candidates into free lanes (evaluating pending
+                // ones whenever every lane is occupied)
                 while (cm) {
-                    const int src = __ffs(cm) - 1;
-                    cm &= cm - 1;
-                    const uint32_t g = __shfl_sync(0xFFFFFFFFu, gid, src);
-                    const double u = __shfl_sync(0xFFFFFFFFu, ub, src);
-                    if (u >= best) {  // best only grows: re-check
-                        const double s = cand_dot(p.idx, p.val, beg, end, p.CT, p.ld_ct, g, lane, fold);
-                        stat(4, 1u);
-                        stat(5, end - beg);
-                        if (s > best || (s == best && g < arg)) {
-                            best = s;
-                            arg = g;
+                    drain(false);
+                    const unsigned fr = ~__ballot_sync(0xFFFFFFFFu, c_on);
+                    const int dst_rank = __popc(fr & ((1u << lane) - 1u));  // this free lane's rank
+                    const int take_n = min(__popc(fr), __popc(cm));
+                    // the r-th remaining candidate goes to the r-th free lane
+                    int src = -1;
+                    if ((fr >> lane) & 1u) {
+                        if (dst_rank < take_n) {
+                            unsigned m = cm;
+                            for (int r = 0; r < dst_rank; ++r) m &= m - 1;
+                            src = __ffs(m) - 1;
                         }
                     }
+                    const uint32_t g2 = __shfl_sync(0xFFFFFFFFu, gid, src < 0 ? 0 : src);
+                    const double u2 = __shfl_sync(0xFFFFFFFFu, ub, src < 0 ? 0 : src);
+                    if (src >= 0) {
+                        c_gid = g2;
+                        c_ub = u2;
+                        c_on = true;
+                    }
+                    for (int r = 0; r < take_n; ++r) cm &= cm - 1;
                 }
             }
+            drain(true);
             if (lane == 0) {
                 p.a[i] = arg;
                 p.sims[i] = best;
@@ -438,11 +494,12 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
 // High postings of the cluster tile [c0, c0 + kt) of M in one pass over M:
 // per term, the (column, value) pairs with |value| ≥ thr in ascending column,
 // at a block-reserved offset (one atomic per 8 terms). Lists land in any order;
-// hptr[t] = (first pair, count). Pairs beyond `cap` are not written (the host
-// grows the buffer and rebuilds when *total > cap).
+// hptr[t] = (first pair, count, largest |value| below thr, 0). Pairs beyond
+// `cap` are not written (the host grows the buffer and rebuilds when
+// *total > cap).
 __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
                                                            uint32_t c0, uint32_t kt, float thr,
-                                                           uint2* __restrict__ hptr, uint2* __restrict__ pairs,
+                                                           uint4* __restrict__ hptr, uint2* __restrict__ pairs,
                                                            unsigned long long cap, unsigned long long* total) {
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_base;
@@ -452,10 +509,20 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
         const uint64_t t = tb + warp;
         const float* row = M + t * ld + c0;
         uint32_t cnt = 0;
+        float lowmax = 0.f;
         if (t < d)
-            for (uint32_t j = lane; j < kt; j += kWarp) cnt += post_keep(row[j], thr);
+            for (uint32_t j = lane; j < kt; j += kWarp) {
+                const float a = fabsf(row[j]);
+                if (post_keep(row[j], thr))
+                    ++cnt;
+                else
+                    lowmax = fmaxf(lowmax, a);
+            }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
+        for (int off = 16; off > 0; off >>= 1) {
+            cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
+            lowmax = fmaxf(lowmax, __shfl_xor_sync(0xFFFFFFFFu, lowmax, off));
+        }
         if (lane == 0) s_cnt[warp] = cnt;
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -468,7 +535,7 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
         unsigned long long b = s_base;
         for (int q = 0; q < warp; ++q) b += s_cnt[q];
         if (t < d) {
-            if (lane == 0) hptr[t] = make_uint2(static_cast<uint32_t>(b), cnt);
+            if (lane == 0) hptr[t] = make_uint4(static_cast<uint32_t>(b), cnt, __float_as_uint(lowmax), 0u);
             if (cnt > 0 && b + cnt <= cap) {
                 uint32_t run = 0;
                 for (uint32_t j0 = 0; j0 < kt; j0 += kWarp) {

@@ -1287,6 +1287,7 @@ private:
             p.c0 = c0;
             p.kt = kt;
             p.first = c0 == 0 ? 1 : 0;
+            p.single_tile = ncols <= KT ? 1 : 0;
             CK(cudaEventRecord(ev_[6], stream_));
             if (KT == 1024)
                 bound_launch<1024>(p, init);
@@ -1735,7 +1736,7 @@ private:
     bool bound_ok_ = false;  // nnz < 2^32 on this device
     DevBuf<uint8_t> btake_, same_;
     DevBuf<uint32_t> bcol_of_;
-    DevBuf<uint2> hptr_;
+    DevBuf<uint4> hptr_;
     DevBuf<unsigned long long> bctr_, hpctr_;
     // ncc+index accounting (index_account)
     DevBuf<uint32_t> ix_cnt_, ix_mval_, ix_jlen_, ix_lcnt_, ix_lptr_, ix_fill_, ix_list_;
