@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         if (lane == 0) sm_st_u32(s_cnt, 0u);
         __syncwarp();
         double s_own = 0.0;
+        int accmax = 0;      // ≥ every accumulator's final value (0: untouched clusters)
         float lowsum = 0.f;  // Σ |x_t|·(largest low |weight| of term t): bounds every cluster's low part
         bool pref_done = false;
         if (active) {
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                             const int qv = __float2int_rn(xs * __uint_as_float(pr[q].y));
                             if (qv != 0) {
                                 const int old = sm_atom_add(s_acc + 4u * pr[q].x, qv);
+                                accmax = max(accmax, old + qv);  // every final value is some old + qv
                                 if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
                                     const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
                                     if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr[q].x);
@@ -389,13 +391,15 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             active = take;
         }
         const bool dense = ntouch > static_cast<uint32_t>(kCap);
+        accmax = __reduce_max_sync(0xFFFFFFFFu, accmax);
         if (active) {
             // candidates: touched clusters whose upper bound reaches the running
             // best, gathered 32 at a time (one per lane) and evaluated in
             // descending bound order, so the likely winner raises `best` first
             // and prunes the rest (a bound below best cannot win or tie)
             const double bx = fmin(low, theta_x1) + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
-            const uint32_t count = dense ? p.kt : ntouch;
+            // no touched cluster can reach best: nothing to evaluate
+            const uint32_t count = static_cast<double>(accmax) * kFixUnit + bx >= best ? (dense ? p.kt : ntouch) : 0u;
             uint32_t c_gid = 0;   // this lane's pending candidate
             double c_ub = -1e300;
             bool c_on = false;

@@ -275,15 +275,25 @@ __global__ void write_cols_kernel(const long long* __restrict__ S, float* __rest
     const double inv = 1.0 / nrm;
     const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
     double dr = 0.0;
-#pragma unroll 4
-    for (uint32_t t = t0; t < t1; ++t) {
-        const uint64_t o = static_cast<uint64_t>(t) * ld + j;
-        const long long q = S[o];
-        const float old = CT[o];
-        const float cn = q == 0 ? 0.f : static_cast<float>(static_cast<double>(q) * inv);
-        const double diff = static_cast<double>(cn) - static_cast<double>(old);
-        dr = fma(diff, diff, dr);
-        if (cn != old) CT[o] = cn;
+    // 8 rows per step, all loads issued before any store (the compiler cannot
+    // prove the Cᵀ store of one row does not alias the next row's load)
+    constexpr int kB = 8;
+    for (uint32_t tb = t0; tb < t1; tb += kB) {
+        long long q[kB];
+        float old[kB];
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+            const uint64_t o = static_cast<uint64_t>(tb + r) * ld + j;
+            q[r] = tb + r < t1 ? __ldcs(S + o) : 0;
+            old[r] = tb + r < t1 ? CT[o] : 0.f;
+        }
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+            const float cn = q[r] == 0 ? 0.f : static_cast<float>(static_cast<double>(q[r]) * inv);
+            const double diff = static_cast<double>(cn) - static_cast<double>(old[r]);
+            dr = fma(diff, diff, dr);
+            if (cn != old[r]) CT[static_cast<uint64_t>(tb + r) * ld + j] = cn;
+        }
     }
     part[static_cast<uint64_t>(rb) * n_ids + c] = dr;
 }
