@@ -1,0 +1,96 @@
+"""The bound screen's result does not depend on θ (bound_kernels.cuh header).
+
+θ only moves work between the high pairs, the candidate dots and the exact
+scan, so every θ — including the degenerate ones (θ tiny: nearly every weight
+high, dense touched sweeps; θ huge: no high pairs, every document falls
+through to the exact tile scan) — and the postings screen (SSKM_BOUND=0) must
+produce bit-identical trajectories. Checked on one cluster tile and on two
+(k > 2048), on nonnegative and signed corpora, in baseline and NCC modes;
+the default run is also teacher-forced against the oracle.
+"""
+import numpy as np
+import pytest
+
+import paper_2108_00895_b200 as P
+from oracle import oracle as O
+from paper_2108_00895_b200 import synthetic as S
+from tests._util import csr_from_rows, random_unit_rows
+
+pytestmark = pytest.mark.gpu
+
+
+def trajectory(m, k, seeds, mode, iters):
+    eng = P.Engine(0)
+    eng.upload(m)
+    eng.configure(k, mode=mode, conv_sq_dist=1e-300, max_iters=iters)
+    eng.init_from_seeds(seeds)
+    out = []
+    for _ in range(iters):
+        st = eng.step()
+        a, s, _ = eng.get_state()
+        out.append((a.copy(), s.copy(), st.dot_products, st.n_reassigned))
+    return out, eng
+
+
+def assert_same(t0, t1, label):
+    assert len(t0) == len(t1)
+    for it, (x, y) in enumerate(zip(t0, t1)):
+        assert np.array_equal(x[0], y[0]), f"{label}: assignments differ at iteration {it + 1}"
+        assert np.array_equal(x[1], y[1]), f"{label}: sims differ at iteration {it + 1}"
+        assert x[2:] == y[2:], f"{label}: counters differ at iteration {it + 1}"
+
+
+def signed_corpus(n, dims, seed):
+    rows = random_unit_rows(np.random.default_rng(seed), n, dims, 30, allow_negative=True)
+    rows = [[(d, float(np.float32(w))) for d, w in r] for r in rows]
+    return P.CorpusMatrix.from_csr(*csr_from_rows(rows, dims=dims, dtype=np.float32))
+
+
+CASES = {
+    "one_tile": lambda: (S.generate(3000, 4096, 24, 60.0, seed=11), 64),
+    "two_tiles": lambda: (S.generate(6000, 8192, 300, 50.0, seed=12), 2100),
+    "signed": lambda: (signed_corpus(2500, 800, 5), 40),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("mode", ["baseline", "ncc"])
+def test_theta_and_screen_invariance(case, mode, monkeypatch):
+    m, k = CASES[case]()
+    seeds = np.random.default_rng(0).choice(m.n_docs, k, replace=False)
+    iters = 5
+    ref, _ = trajectory(m, k, seeds, mode, iters)
+    for theta in ("1e-5", "0.02", "0.3"):
+        monkeypatch.setenv("SSKM_THETA", theta)
+        t, _ = trajectory(m, k, seeds, mode, iters)
+        assert_same(ref, t, f"theta={theta}")
+    monkeypatch.delenv("SSKM_THETA")
+    monkeypatch.setenv("SSKM_BOUND", "0")
+    t, _ = trajectory(m, k, seeds, mode, iters)
+    assert_same(ref, t, "postings screen")
+
+
+def test_bound_default_teacher_forced_against_oracle():
+    """Default (adaptive θ) bound screen vs the oracle's assign on the GPU's
+    centroids and state, bitwise, on two cluster tiles."""
+    m, k = CASES["two_tiles"]()
+    seeds = np.random.default_rng(0).choice(m.n_docs, k, replace=False)
+    eng = P.Engine(0)
+    eng.upload(m)
+    eng.configure(k, mode="baseline", conv_sq_dist=1e-300, max_iters=10)
+    eng.init_from_seeds(seeds)
+    c = O.Corpus(m.indptr, m.indices, m.values.astype(np.float64), m.dims)
+    ref = O.Stepper(c, k, "baseline", kind="ref" if O.ref_available() else "port")
+    for it in range(1, 5):
+        eng.update()
+        a_mid, s_mid, unch = eng.get_state()
+        ct = eng.get_centroids()
+        st = eng.assign()
+        assert st.bound_docs > 0 or it == 1
+        a, s, _ = eng.get_state()
+        ref.set_centroids_dense(ct)
+        ref.set_state(a_mid, s_mid, unch, it)
+        ref.assign()
+        ra, rs, _ = ref.get_state()
+        assert np.array_equal(ra, a), it
+        assert np.array_equal(rs, s), it
