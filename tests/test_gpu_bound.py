@@ -20,6 +20,7 @@ pytestmark = pytest.mark.gpu
 
 
 def trajectory(m, k, seeds, mode, iters):
+    thetas = []
     eng = P.Engine(0)
     eng.upload(m)
     eng.configure(k, mode=mode, conv_sq_dist=1e-300, max_iters=iters)
@@ -29,7 +30,8 @@ def trajectory(m, k, seeds, mode, iters):
         st = eng.step()
         a, s, _ = eng.get_state()
         out.append((a.copy(), s.copy(), st.dot_products, st.n_reassigned))
-    return out, eng
+        thetas.append(st.bound_theta)
+    return out, thetas
 
 
 def assert_same(t0, t1, label):
@@ -62,12 +64,15 @@ def test_theta_and_screen_invariance(case, mode, monkeypatch):
     ref, _ = trajectory(m, k, seeds, mode, iters)
     for theta in ("1e-5", "0.02", "0.3"):
         monkeypatch.setenv("SSKM_THETA", theta)
-        t, _ = trajectory(m, k, seeds, mode, iters)
+        t, th = trajectory(m, k, seeds, mode, iters)
         assert_same(ref, t, f"theta={theta}")
+        # the fixed split was the one used (passes that ran the bound screen)
+        assert any(x > 0 for x in th) and all(x == 0 or x == pytest.approx(float(theta), rel=1e-6) for x in th)
     monkeypatch.delenv("SSKM_THETA")
     monkeypatch.setenv("SSKM_BOUND", "0")
-    t, _ = trajectory(m, k, seeds, mode, iters)
+    t, th = trajectory(m, k, seeds, mode, iters)
     assert_same(ref, t, "postings screen")
+    assert all(x == 0 for x in th)  # no bound-screen pass ran
 
 
 def test_bound_default_teacher_forced_against_oracle():
