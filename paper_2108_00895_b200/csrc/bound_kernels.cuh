@@ -320,34 +320,48 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     ext = ld_u4_nc(p.hptr + t);
                     if (need_dot) cv = ld_f32_nc(p.CT + static_cast<uint64_t>(t) * p.ld_ct + arg);
                 }
-                // the term's high pairs, up to 4 per round with their loads in
-                // flight together (lists average ~1 pair on the TF-IDF corpora);
-                // longer lists loop on in the lanes that have them
+                // the chunk's high pairs, flattened into windows of 32 slots (one
+                // pair per lane, all loads of a window in flight together); slot
+                // s belongs to the first lane whose inclusive prefix exceeds s,
+                // found by a 5-step binary search over the lanes' prefixes
                 const uint32_t cnt = ext.y;
-                const float xs = x * kFixScale;
                 lowsum = fmaf(fabsf(x), __uint_as_float(ext.z), lowsum);
-                for (uint32_t k0 = 0; k0 < cnt; k0 += 4) {
-                    uint2 pr[4];
+                uint32_t incl = cnt;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        pr[q] = k0 + q < cnt ? ld_pair(pairs + ext.x + k0 + q, pol_keep) : make_uint2(kNone, 0u);
+                for (int off = 1; off < kWarp; off <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+                    if (lane >= off) incl += o;
+                }
+                const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, kWarp - 1);
+                const uint32_t adj = ext.x - (incl - cnt);  // pair index = adj + slot
+                const float xs = x * kFixScale;
+                for (uint32_t wb = 0; wb < total; wb += kWarp) {
+                    const uint32_t sl = wb + lane;
+                    int lo = 0;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (pr[q].x != kNone && pr[q].x != own_l) {
-                            const int qv = __float2int_rn(xs * __uint_as_float(pr[q].y));
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, lo + step - 1);
+                        if (v <= sl) lo += step;
+                    }
+                    const uint32_t base_o = __shfl_sync(0xFFFFFFFFu, adj, lo & (kWarp - 1));
+                    const float xs_o = __shfl_sync(0xFFFFFFFFu, xs, lo & (kWarp - 1));
+                    if (sl < total) {
+                        const uint2 pr = ld_pair(pairs + (base_o + sl), pol_keep);
+                        if (pr.x != own_l) {
+                            const int qv = __float2int_rn(xs_o * __uint_as_float(pr.y));
                             if (qv != 0) {
-                                const int old = sm_atom_add(s_acc + 4u * pr[q].x, qv);
+                                const int old = sm_atom_add(s_acc + 4u * pr.x, qv);
                                 accmax = max(accmax, old + qv);  // every final value is some old + qv
                                 if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
                                     const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
-                                    if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr[q].x);
+                                    if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr.x);
                                 }
                             }
                         }
                     }
                 }
                 __syncwarp();
-                stat(2, __reduce_add_sync(0xFFFFFFFFu, cnt));
+                stat(2, total);
                 if (need_dot)  // own dot, ascending entry order, exact in fp64
                     s_own = fold_chunk(s_own, cvt_f64(x) * cvt_f64(cv), static_cast<int>(min(32u, end - e0)), lane,
                                        fold);
@@ -514,14 +528,25 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
         const float* row = M + t * ld + c0;
         uint32_t cnt = 0;
         float lowmax = 0.f;
-        if (t < d)
-            for (uint32_t j = lane; j < kt; j += kWarp) {
-                const float a = fabsf(row[j]);
-                if (post_keep(row[j], thr))
-                    ++cnt;
-                else
-                    lowmax = fmaxf(lowmax, a);
+        if (t < d) {
+            // 16-byte loads over the row (tiles start at multiples of 4 columns)
+            const uint32_t kt4 = kt & ~3u;
+            for (uint32_t j = 4u * lane; j < kt4; j += 4u * kWarp) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
+                const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const bool k = post_keep(e[r], thr);
+                    cnt += k;
+                    lowmax = k ? lowmax : fmaxf(lowmax, fabsf(e[r]));
+                }
             }
+            for (uint32_t j = kt4 + lane; j < kt; j += kWarp) {
+                const bool k = post_keep(row[j], thr);
+                cnt += k;
+                lowmax = k ? lowmax : fmaxf(lowmax, fabsf(row[j]));
+            }
+        }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
