@@ -246,9 +246,11 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     if (w + nwarps < w1) i_nn = doc_of(w + nwarps);
     int32_t t_n = 0;
     float x_n = 0.f;
+    uint4 ext_n = make_uint4(0u, 0u, 0u, 0u);  // the prefetched chunk's postings extents
     if (w < w1 && beg_n + lane < end_n) {
         t_n = ld_stream_i32(p.idx + beg_n + lane, pol_stream);
         x_n = ld_stream_f32(p.val + beg_n + lane, pol_stream);
+        ext_n = ld_u4_nc(p.hptr + t_n);
     }
     for (; w < w1; w += nwarps) {
         const uint32_t i = i_n, beg = beg_n, end = end_n;
@@ -298,28 +300,26 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 const bool valid = e0 + lane < end;
                 const int32_t t = t_n;
                 const float x = x_n;
+                const uint4 ext = ext_n;  // issued one chunk earlier
                 // the next chunk first (this document's, else the next document's),
                 // so its loads fly while this chunk waits on its own
+                bool nv;
                 {
                     const bool last = e0 + kWarp >= end;
                     const uint32_t en = last ? beg_n + lane : e0 + kWarp + lane;
                     const uint32_t lim = last ? (wn < w1 ? end_n : 0u) : end;
+                    nv = en < lim;
                     t_n = 0;
                     x_n = 0.f;
-                    if (en < lim) {
+                    if (nv) {
                         t_n = ld_stream_i32(p.idx + en, pol_stream);
                         x_n = ld_stream_f32(p.val + en, pol_stream);
                     }
                     if (last) pref_done = true;
                 }
-                // this chunk's postings extent and own-column weight (the weight
-                // is first used by the fold, after the pairs)
-                uint4 ext = make_uint4(0u, 0u, 0u, 0u);
+                // this chunk's own-column weight (first used by the fold, after the pairs)
                 float cv = 0.f;
-                if (valid) {
-                    ext = ld_u4_nc(p.hptr + t);
-                    if (need_dot) cv = ld_f32_nc(p.CT + static_cast<uint64_t>(t) * p.ld_ct + arg);
-                }
+                if (valid && need_dot) cv = ld_f32_nc(p.CT + static_cast<uint64_t>(t) * p.ld_ct + arg);
                 // the chunk's high pairs, flattened into windows of 32 slots (one
                 // pair per lane, all loads of a window in flight together); slot
                 // s belongs to the first lane whose inclusive prefix exceeds s,
@@ -360,6 +360,9 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                         }
                     }
                 }
+                // the next chunk's extents, now that its terms have arrived: in
+                // flight during this chunk's fold and the loop turn
+                ext_n = nv ? ld_u4_nc(p.hptr + t_n) : make_uint4(0u, 0u, 0u, 0u);
                 __syncwarp();
                 stat(2, total);
                 if (need_dot)  // own dot, ascending entry order, exact in fp64
@@ -370,9 +373,11 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         if (!pref_done) {  // empty or skipped document: prefetch the next one's first chunk
             t_n = 0;
             x_n = 0.f;
+            ext_n = make_uint4(0u, 0u, 0u, 0u);
             if (wn < w1 && beg_n + lane < end_n) {
                 t_n = ld_stream_i32(p.idx + beg_n + lane, pol_stream);
                 x_n = ld_stream_f32(p.val + beg_n + lane, pol_stream);
+                ext_n = ld_u4_nc(p.hptr + t_n);
             }
         }
         __syncwarp();
