@@ -971,10 +971,15 @@ __global__ void finish_assign_kernel(const uint32_t* __restrict__ a, const uint3
     }
 }
 
+// Σ part[0..n) in index order (one thread), the partials staged in shared
+// memory by the block first (n ≤ 4096).
 __global__ void sum_parts_kernel(const double* __restrict__ part, int n, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
+    __shared__ double sh[4096];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sh[i] = part[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
         double s = 0.0;
-        for (int i = 0; i < n; ++i) s += part[i];
+        for (int i = 0; i < n; ++i) s += sh[i];
         *out = s;
     }
 }

@@ -389,8 +389,6 @@ public:
             touched_.p, Q_.p);
         CK_LAUNCH();
         finish_update(st);
-        CK(cudaEventRecord(ev_[1], stream_));
-        CK(cudaEventSynchronize(ev_[1]));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
         st->update_ms = ms;
@@ -419,8 +417,6 @@ public:
             CK_LAUNCH();
         }
         finish_update(st);
-        CK(cudaEventRecord(ev_[1], stream_));
-        CK(cudaEventSynchronize(ev_[1]));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
         st->update_ms = ms;
@@ -641,7 +637,7 @@ public:
         uint64_t n_exact = 0;
         if (screen_enabled_) {
             if (!screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_, kInitFull)) resolve<kInitFull>(order, n_);
-            pull_scalars();
+            pull_scalars_unless_fresh();
             n_exact = hs_->n_exact;
             if (n_exact > 0) scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(n_exact));
         } else {
@@ -674,7 +670,7 @@ public:
                                 static_cast<double>(n_chg_) >= ncc_full_frac_ * k_;
         if (n_chg_ > 0 && full_equiv) {
             if (!screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_, kInitFull)) resolve<kInitFull>(order, n_);
-            pull_scalars();
+            pull_scalars_unless_fresh();
             n_exact = hs_->n_exact;
             if (n_exact > 0) scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(n_exact));
             CK(cudaMemsetAsync(&scal_.p->n_rescan, 0, 8, stream_));
@@ -687,7 +683,7 @@ public:
             if (screen_enabled_) {
                 if (!screen_any(cc_.p, ld_cc_, n_chg_, chg_ids_.p, a_start_.p, order, n_, kInitNcc))
                     resolve<kInitNcc>(order, n_);
-                pull_scalars();
+                pull_scalars_unless_fresh();
                 n_exact = hs_->n_exact;
                 if (n_exact > 0)
                     scan_tiles<kInitNcc>(cc_.p, ld_cc_, n_chg_, chg_ids_.p, exact_.p, static_cast<int64_t>(n_exact));
@@ -702,7 +698,7 @@ public:
                     CK(cudaMemsetAsync(&scal_.p->n_exact, 0, 8, stream_));
                     if (!screen_any(ct_.p, ld_, k_, nullptr, a_.p, rescan_.p, static_cast<int64_t>(n_rescan), kInitRescan))
                         resolve<kInitRescan>(rescan_.p, static_cast<int64_t>(n_rescan));
-                    pull_scalars();
+                    pull_scalars_unless_fresh();
                     const uint64_t nx = hs_->n_exact;
                     n_exact += nx;
                     if (nx > 0) scan_tiles<kInitRescan>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(nx));
@@ -916,7 +912,7 @@ public:
     double local_sims_sum() {
         need_state();
         launch(local_sum_kernel, kObjBlocks, 256, sims_.p, n_, obj_part_.p);
-        launch(sum_parts_kernel, 1, 32, obj_part_.p, kObjBlocks, &scal_.p->objective);
+        launch(sum_parts_kernel, 1, 256, obj_part_.p, kObjBlocks, &scal_.p->objective);
         CK_LAUNCH();
         pull_scalars();
         return hs_->objective;
@@ -946,6 +942,12 @@ private:
     void pull_scalars() {
         CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
+    }
+    // The bound screen pulls the scalars with its own counters (one sync); the
+    // call right after a screen then has nothing to wait for.
+    void pull_scalars_unless_fresh() {
+        if (!scalars_fresh_) pull_scalars();
+        scalars_fresh_ = false;
     }
 
     // All per-iteration scratch is sized once here, so no cudaMalloc (and its
@@ -1098,21 +1100,21 @@ private:
 
     // Renormalise touched columns, drift, unchanged flags, changed list.
     void finish_update(sskm_iteration_stats* st) {
-        // touched clusters, ascending
+        // touched clusters, ascending; their count stays on the device (the
+        // column kernels are sized for k and read it there)
         launch(compact_ids_kernel, 1, 1024, touched_.p, k_, 1, rec_ids_.p, &scal_.p->n_rec);
         CK_LAUNCH();
-        pull_scalars();
-        const uint32_t n_rec = hs_->n_rec;
         const uint32_t n_rb = static_cast<uint32_t>(ceil_div(d_, kRowBlock));
-        if (n_rec > 0) {
-            dim3 grid(static_cast<unsigned>(ceil_div(n_rec, 128)), n_rb);
-            launch(q_norm2_kernel, static_cast<unsigned>(ceil_div(n_rec, 128)), 128, Q_.p, rec_ids_.p, n_rec,
+        const unsigned* n_rec_dev = &scal_.p->n_rec;
+        {
+            dim3 grid(static_cast<unsigned>(ceil_div(k_, 128)), n_rb);
+            launch(q_norm2_kernel, static_cast<unsigned>(ceil_div(k_, 128)), 128, Q_.p, rec_ids_.p, n_rec_dev,
                    norm2_.p);
-            launch(write_cols_kernel, grid, 128, S_.p, ct_.p, ld_, d_, rec_ids_.p, n_rec, norm2_.p,
-                                                         part_.p, &scal_.p->zero_flag);
-            launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(n_rec, 128)), 128, 
-                part_.p, n_rb, n_rec, drift_rec_.p);
-            launch(scatter_pos_kernel, grid_for(n_rec, 256), 256, rec_ids_.p, n_rec, rec_pos_.p);
+            launch(write_cols_kernel, grid, 128, S_.p, ct_.p, ld_, d_, rec_ids_.p, n_rec_dev, k_, norm2_.p, part_.p,
+                   &scal_.p->zero_flag);
+            launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 256, part_.p, n_rb, n_rec_dev, k_,
+                   drift_rec_.p);
+            launch(scatter_pos_dev_kernel, grid_for(k_, 256), 256, rec_ids_.p, n_rec_dev, rec_pos_.p);
             CK_LAUNCH();
         }
         launch(flags_kernel, grid_for(k_, 256), 256, 
@@ -1121,7 +1123,9 @@ private:
         CK_LAUNCH();
         CK(cudaMemsetAsync(touched_.p, 0, k_, stream_));
         ++updates_since_assign_;
+        CK(cudaEventRecord(ev_[1], stream_));  // end of the update (timed by the caller)
         pull_scalars();
+        const uint32_t n_rec = hs_->n_rec;
         if (hs_->zero_flag) throw InvalidArgument("cannot normalize zero vector");
         n_unchanged_ = hs_->n_unchanged;
         // rewritten columns are fp32 roundings of unit vectors: ||c|| <= 1 + 2^-23
@@ -1239,7 +1243,7 @@ private:
         CK(cudaMemsetAsync(bctr_.p, 0, 8 * sizeof(unsigned long long), stream_));
         const float thr = theta_adapt_ ? tctl_[init].theta : theta_;
         const uint32_t KT = ncols <= 1024 ? 1024 : 2048;
-        double pass_ms = 0.0;
+        double pass_ms = 0.0, build_ms_inner = 0.0;
         BoundArgs p{};
         p.indptr = indptr_.p;
         p.indptr32 = indptr32_.p;
@@ -1281,36 +1285,49 @@ private:
         }
         for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
             const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
-            build_hipost(M, ld, c0, kt, thr);
+            if (c0 > 0) CK(cudaEventRecord(ev_[8], stream_));
+            build_hipost(M, ld, c0, kt, thr);  // synchronises (capacity check)
+            if (c0 > 0) {
+                CK(cudaEventRecord(ev_[9], stream_));
+                CK(cudaEventSynchronize(ev_[9]));
+                float bms = 0.f;
+                CK(cudaEventElapsedTime(&bms, ev_[8], ev_[9]));
+                build_ms_inner += bms;
+            }
             p.hptr = hptr_.p;
             p.pairs = pairs_.p;
             p.c0 = c0;
             p.kt = kt;
             p.first = c0 == 0 ? 1 : 0;
             p.single_tile = ncols <= KT ? 1 : 0;
-            CK(cudaEventRecord(ev_[6], stream_));
+            // the screen launches are timed as one interval: the event pair
+            // brackets every tile's screen, and the postings builds between
+            // tiles are timed separately (build_ms) and subtracted
+            if (c0 == 0) CK(cudaEventRecord(ev_[6], stream_));
             if (KT == 1024)
                 bound_launch<1024>(p, init);
             else
                 bound_launch<2048>(p, init);
-            CK(cudaEventRecord(ev_[7], stream_));
-            CK(cudaEventSynchronize(ev_[7]));
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
-            screen_ms_ += ms;
-            pass_ms += ms;
             screen_launches_ += 1;
         }
+        CK(cudaEventRecord(ev_[7], stream_));
         if (init == kInitNcc)
             launch(bound_ncc_rescan_kernel, grid_for(n_work, 256), 256, order, n_work, btake_.p, a_start_.p,
                    sims_start_.p, sims_.p, unchanged_.p, rescan_.p, &scal_.p->n_rescan);
         // θ for the next assign: keep the exact-scan share small and the
         // candidate dots near one per document (θ never changes a result)
         unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
-        uint64_t n_fb = 0;
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
-        CK(cudaMemcpyAsync(&n_fb, &scal_.p->n_exact, 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
+        scalars_fresh_ = true;
+        const uint64_t n_fb = hs_->n_exact;
+        {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
+            pass_ms = static_cast<double>(ms) - build_ms_inner;
+            screen_ms_ += pass_ms;
+        }
         const uint64_t n_list = n_work > 0 ? static_cast<uint64_t>(n_work) - std::min<uint64_t>(n_fb, n_work) : 0;
         bstat_docs_ += n_list;
         bstat_pairs_ += ctr[1];
@@ -1669,7 +1686,7 @@ private:
         reset_scalars_keep_rescan();
         launch(finish_assign_kernel, kObjBlocks, 256, a_.p, a_start_.p, sims_.p, n_, obj_part_.p,
                                                               &scal_.p->reassigned);
-        launch(sum_parts_kernel, 1, 32, obj_part_.p, kObjBlocks, &scal_.p->objective);
+        launch(sum_parts_kernel, 1, 256, obj_part_.p, kObjBlocks, &scal_.p->objective);
         CK_LAUNCH();
         CK(cudaEventRecord(ev_[3], stream_));
         pull_scalars();
@@ -1705,7 +1722,7 @@ private:
     int device_;
     int sms_ = 148;
     cudaStream_t stream_{};
-    cudaEvent_t ev_[8]{};
+    cudaEvent_t ev_[10]{};
     static constexpr int kUserEvents = 16;
     cudaEvent_t user_ev_[kUserEvents]{};
     uint64_t launches_ = 0;
@@ -1763,6 +1780,7 @@ private:
     uint32_t post_kt_max_ = 1024;
     int post_warps_ = 8;
     bool cache_trusted_ = false;
+    bool scalars_fresh_ = false;  // hs_ was pulled by the last bound-screen pass
     bool fuse_resolve_ = false;
     bool bound_enabled_ = true;   // bound screen (SSKM_BOUND=0: the full postings / dense screens)
     bool theta_adapt_ = true;

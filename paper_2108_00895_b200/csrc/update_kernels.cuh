@@ -157,8 +157,10 @@ __global__ void delta_packed_kernel(int64_t n_moved, const uint32_t* __restrict_
 }
 
 // ‖S_j‖² of the recomputed columns from the exact 128-bit Q_j (< 2^124, ≥ 0).
+// The column count n is read on the device (no host round trip).
 __global__ void q_norm2_kernel(const unsigned long long* __restrict__ Q, const uint32_t* __restrict__ ids,
-                               uint32_t n_ids, double* __restrict__ norm2) {
+                               const unsigned int* __restrict__ n_dev, double* __restrict__ norm2) {
+    const uint32_t n_ids = *n_dev;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_ids; c += gridDim.x * blockDim.x) {
         const uint32_t j = ids[c];
         const unsigned long long lo = Q[2ull * j], hi = Q[2ull * j + 1];
@@ -246,13 +248,30 @@ __global__ void compact_ids_kernel(const uint8_t* __restrict__ flags, uint32_t k
 
 constexpr int kRowBlock = 512;  // rows per partial in the column reductions
 
-__global__ void reduce_partials_kernel(const double* __restrict__ part, uint32_t n_rb,
-                                       uint32_t n_ids, double* __restrict__ out) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= n_ids) return;
+// Column sums of the row-block partials part[rb][c] (row stride `stride`), in
+// a fixed association: 8 segments of row blocks summed in order by 8 threads
+// of a column, then the 8 segment sums in order. Deterministic; 32 columns per
+// 256-thread block.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ part, uint32_t n_rb,
+                                                              const unsigned int* __restrict__ n_dev,
+                                                              uint32_t stride, double* __restrict__ out) {
+    __shared__ double sh[8][32];
+    const uint32_t n_ids = *n_dev;
+    const uint32_t cl = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const uint32_t c = blockIdx.x * 32 + cl;
+    const uint32_t per = (n_rb + 7) / 8;
     double s = 0.0;
-    for (uint32_t rb = 0; rb < n_rb; ++rb) s += part[static_cast<uint64_t>(rb) * n_ids + c];
-    out[c] = s;
+    if (c < n_ids)
+        for (uint32_t rb = seg * per; rb < min(n_rb, (seg + 1) * per); ++rb)
+            s += part[static_cast<uint64_t>(rb) * stride + c];
+    sh[seg][cl] = s;
+    __syncthreads();
+    if (seg == 0 && c < n_ids) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += sh[q][cl];
+        out[c] = t;
+    }
 }
 
 // Rewrite recomputed columns: c = S · (1/||S||) in fp64, stored fp32, with the
@@ -261,11 +280,12 @@ __global__ void reduce_partials_kernel(const double* __restrict__ part, uint32_t
 // 160-209; both land within one fp64 ulp, below fp32 resolution.)
 __global__ void write_cols_kernel(const long long* __restrict__ S, float* __restrict__ CT,
                                   uint64_t ld, uint32_t d, const uint32_t* __restrict__ ids,
-                                  uint32_t n_ids, const double* __restrict__ norm2,
-                                  double* __restrict__ part, unsigned int* zero_flag) {
+                                  const unsigned int* __restrict__ n_dev, uint32_t stride,
+                                  const double* __restrict__ norm2, double* __restrict__ part,
+                                  unsigned int* zero_flag) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t rb = blockIdx.y;
-    if (c >= n_ids) return;
+    if (c >= *n_dev) return;
     const uint32_t j = ids[c];
     const double nrm = sqrt(norm2[c]);
     if (nrm == 0.0) {  // normalize() of the zero vector throws (sparse_vector.cpp:161)
@@ -295,7 +315,7 @@ __global__ void write_cols_kernel(const long long* __restrict__ S, float* __rest
             if (cn != old[r]) CT[static_cast<uint64_t>(tb + r) * ld + j] = cn;
         }
     }
-    part[static_cast<uint64_t>(rb) * n_ids + c] = dr;
+    part[static_cast<uint64_t>(rb) * stride + c] = dr;
 }
 
 // Repair candidates: (orderable(sim), doc) keys for one stable radix sort.
@@ -348,6 +368,13 @@ __global__ void flags_kernel(uint32_t k, int first_iter, double eps, const uint8
 }
 
 __global__ void scatter_pos_kernel(const uint32_t* __restrict__ ids, uint32_t n, uint32_t* __restrict__ pos) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+        pos[ids[c]] = c;
+}
+
+__global__ void scatter_pos_dev_kernel(const uint32_t* __restrict__ ids, const unsigned int* __restrict__ n_dev,
+                                       uint32_t* __restrict__ pos) {
+    const uint32_t n = *n_dev;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
         pos[ids[c]] = c;
 }
