@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         if constexpr (INIT == kInitNcc) return first ? __ldg(p.a_start + i) : p.a[i];
         return p.a[i];
     };
-    auto stat = [&](int k, uint32_t v) {  // per-warp statistics (lane 0)
-        if (lane == 0) sm_st_u32(s_st + 4u * k, sm_ld_u32(s_st + 4u * k) + v);
+    auto stat = [&](int k, uint32_t v) {  // per-warp statistics (lane 0; a reduction, nothing waits on it)
+        if (lane == 0) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(s_st + 4u * k), "r"(v));
     };
     uint32_t w = w0 + warp;
     uint32_t i_n = 0, i_nn = 0, arg_n = 0, beg_n = 0, end_n = 0;
