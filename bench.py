@@ -211,6 +211,27 @@ def bound_screen_bytes(stats):
             "candidate_nnz": cnnz, "theta": m("bound_theta")}
 
 
+def bound_roofline(stats, data):
+    """roofline object of the dominant kernel (bound_screen_kernel) from the
+    steps' own counters and CUDA-event times."""
+    screen_ms = statistics.mean(s.screen_ms for s in stats)
+    bb = bound_screen_bytes(stats)
+    peak, peak_src = measured_peak_gbs()
+    achieved = bb["bytes"] / (screen_ms / 1e3) / 1e9 if screen_ms > 0 else 0.0
+    traffic, _ = ncu_traffic()
+    kk = stats[0].n_changed if stats else 0
+    bytes_dense = algorithmic_assign_bytes(data, max(kk, 1))
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "bound_screen_kernel",
+            "bytes_per_assign": bb["bytes"], "bytes_breakdown": bb, "screen_ms_per_assign": screen_ms,
+            "launches_per_assign": statistics.mean(s.screen_launches for s in stats), "peak_source": peak_src,
+            "dense_equivalent": {"bytes": bytes_dense, "gbs": bytes_dense / (screen_ms / 1e3) / 1e9 if screen_ms else 0,
+                                 "note": "SURVEY 8d B_assign (4·Σ nnz_i·k): what a dense Ct scan would move"},
+            "note": "algorithmic bytes of the bound screen = 8·high pairs + 16·doc nnz read + 36·doc visits "
+                    "+ 4·candidate-dot nnz (DESIGN.md §3.1), over the kernel's CUDA-event time; "
+                    "traffic = ncu dram bytes per launch (profiles/ncu_bound_summary.json)"}
+
+
 def run_ours(args):
     import paper_2108_00895_b200 as P
     from paper_2108_00895_b200 import synthetic as S
@@ -220,7 +241,7 @@ def run_ours(args):
     if world > 1 or args.distributed:
         from paper_2108_00895_b200 import distributed as D
 
-        return D.bench_distributed(args)
+        return D.bench_distributed(args, {"clock": ClockSampler, "roofline": bound_roofline})
     cfg = S.CONFIGS[args.config]
     data = S.corpus(cfg)
     k = cfg.k
@@ -247,14 +268,8 @@ def run_ours(args):
     performed = sum(s.gpu_dot_products for s in stats) / (total_ms / 1e3)
     kern_ms = [s.assign_kernel_ms for s in stats]
     peak, peak_src = measured_peak_gbs()
-    # dominant kernel: the bound screen (bound_screen_kernel, one launch per cluster tile)
-    screen_ms = statistics.mean(s.screen_ms for s in stats)
-    launches_per_assign = statistics.mean(s.screen_launches for s in stats)
-    bb = bound_screen_bytes(stats)
-    achieved = bb["bytes"] / (screen_ms / 1e3) / 1e9
-    pairs_full = eng.postings_work()
-    bytes_dense = algorithmic_assign_bytes(data, k)
-    traffic, ncu = ncu_traffic()
+    roofline = bound_roofline(stats, data)
+    roofline["full_postings_pairs_per_assign"] = eng.postings_work()
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": args.warmup,
@@ -266,18 +281,9 @@ def run_ours(args):
         "phase_ms": {"update": statistics.mean(s.update_ms for s in stats),
                      "assign": statistics.mean(s.assign_ms for s in stats),
                      "assign_kernels": statistics.mean(kern_ms),
-                     "screen": screen_ms},
-        "uncertified_docs_per_iter": statistics.mean(s.n_exact for s in stats),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "bound_screen_kernel",
-                     "bytes_per_assign": bb["bytes"], "bytes_breakdown": bb, "screen_ms_per_assign": screen_ms,
-                     "launches_per_assign": launches_per_assign, "peak_source": peak_src,
-                     "full_postings_pairs_per_assign": pairs_full,
-                     "dense_equivalent": {"bytes": bytes_dense, "gbs": bytes_dense / (screen_ms / 1e3) / 1e9,
-                                          "note": "SURVEY 8d B_assign (4·Σ nnz_i·k): what a dense Ct scan would move"},
-                     "note": "algorithmic bytes of the bound screen = 8·high pairs + 16·doc nnz read + 36·doc visits "
-                             "+ 4·candidate-dot nnz (DESIGN.md §3.1), over the kernel's CUDA-event time; "
-                             "traffic = ncu dram bytes per launch"},
+                     "screen": roofline["screen_ms_per_assign"]},
+        "exact_scan_docs_per_iter": statistics.mean(s.n_exact for s in stats),
+        "roofline": roofline,
         "gpu_launches": launches,
         "clocks": clocks,
     }

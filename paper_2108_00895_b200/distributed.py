@@ -186,6 +186,38 @@ class Comm:
         dist.all_gather(outs, buf, group=self.group)
         return [o[:c].to(src_dev) for o, c in zip(outs, ns)]
 
+    def all_gather_var_multi(self, ts):
+        """All-gather of several 1-D tensors of per-rank length: one gather of
+        all the lengths, then one padded gather per tensor. Returns, per tensor,
+        the rank-ordered list."""
+        import torch
+        dist = self._d()
+        src = [t.device for t in ts]
+        ts = [t.to(self.dev) for t in ts]
+        n = torch.tensor([t.numel() for t in ts], dtype=torch.int64, device=self.dev)
+        ns = torch.zeros(self.world * len(ts), dtype=torch.int64, device=self.dev)
+        dist.all_gather_into_tensor(ns, n, group=self.group)
+        ns = ns.view(self.world, len(ts)).cpu().tolist()
+        res = []
+        for i, t in enumerate(ts):
+            mx = max(max(r[i] for r in ns), 1)
+            buf = torch.zeros(mx, dtype=t.dtype, device=self.dev)
+            buf[: t.numel()] = t
+            out = torch.empty(self.world * mx, dtype=t.dtype, device=self.dev)
+            dist.all_gather_into_tensor(out, buf, group=self.group)
+            out = out.view(self.world, mx)
+            res.append([out[r, : ns[r][i]].to(src[i]) for r in range(self.world)])
+        return res
+
+    def all_gather_f64_vec(self, x: np.ndarray) -> np.ndarray:
+        """[world, len(x)] float64, rank-ordered rows."""
+        import torch
+        dist = self._d()
+        t = torch.as_tensor(np.ascontiguousarray(x, np.float64)).to(self.dev)
+        out = torch.empty(self.world * t.numel(), dtype=torch.float64, device=self.dev)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.view(self.world, -1).cpu().numpy()
+
     def all_gather_object(self, obj) -> list:
         dist = self._d()
         out = [None] * self.world
@@ -286,8 +318,22 @@ class DistributedKMeans:
                 if self.owner(gid) == self.comm.rank:
                     self.s.move_doc(gid, new)
             repaired = [new for _, _, new in moves]
+        import torch
+
         old, new, lens, idx, val = self.s.moved_pack()
-        parts = [self.comm.all_gather_var(t) for t in (old, new, lens, idx, val)]
+        # two payloads: per moved document (old, new, row length), and the rows
+        # (term ids and the fp32 weights' bits): one length gather + two gathers
+        meta = torch.cat([old, new, lens])
+        rows = torch.cat([idx, val.view(torch.int32)])
+        g_meta, g_rows = self.comm.all_gather_var_multi([meta, rows])
+        parts = [[], [], [], [], []]
+        for m_r, r_r in zip(g_meta, g_rows):
+            n_r, z_r = m_r.numel() // 3, r_r.numel() // 2
+            parts[0].append(m_r[:n_r])
+            parts[1].append(m_r[n_r:2 * n_r])
+            parts[2].append(m_r[2 * n_r:])
+            parts[3].append(r_r[:z_r])
+            parts[4].append(r_r[z_r:].view(torch.float32))
         cat = [self._cat(p) for p in parts]
         st = self.s.update_apply(*cat, repaired)
         self.iteration += 1
@@ -309,13 +355,15 @@ class DistributedKMeans:
         # every counter is a sum over documents (the reference's accounting is
         # per document, engine.cpp:244-312), so the global value is the sum of
         # the ranks' local ones — in every mode, the ncc+index replay included
-        tot = self.comm.all_reduce_i64(np.array([st.n_reassigned, st.n_rescan, st.n_exact, st.gpu_dot_products,
-                                                 st.dot_products, st.index_queries, st.candidates_total],
-                                                np.int64))
-        objs = self.comm.all_gather_f64(st.objective)
+        # one gather: the objective partial and the counters (< 2^53: exact in
+        # fp64), summed on the host in rank order
+        g = self.comm.all_gather_f64_vec(np.array([st.objective, st.n_reassigned, st.n_rescan, st.n_exact,
+                                                   st.gpu_dot_products, st.dot_products, st.index_queries,
+                                                   st.candidates_total], np.float64))
+        tot = [int(round(sum(float(v) for v in g[:, c]))) for c in range(1, g.shape[1])]
         obj = 0.0
-        for o in objs:  # rank order: deterministic for a given world size
-            obj += o
+        for o in g[:, 0]:  # rank order: deterministic for a given world size
+            obj += float(o)
         return replace(st, n_reassigned=int(tot[0]), n_rescan=int(tot[1]), n_exact=int(tot[2]),
                        gpu_dot_products=int(tot[3]), objective=obj, dot_products=int(tot[4]),
                        index_queries=int(tot[5]), candidates_total=int(tot[6]))
@@ -354,43 +402,81 @@ def init_process_group_from_env(backend: Optional[str] = None):
     return dist.get_rank(), dist.get_world_size()
 
 
-def bench_distributed(args):
-    """bench.py at N > 1: strong scaling of config args.config over N GPUs."""
+def bench_distributed(args, extras=None):
+    """bench.py at N > 1 (torchrun, one rank per GPU): strong scaling of config
+    args.config over N GPUs. Device time of K steps on every rank's engine
+    stream, max over ranks; clocks sampled on each rank's GPU during the timed
+    region (rank 0 reports its own); e2e = the same K steps through the shard
+    API from host CSR (upload, seeding, steps, download), wall clock max over
+    ranks. `extras` (from bench.py): {"clock": ClockSampler class,
+    "roofline": fn(stats, data) -> roofline dict}."""
     import json
     import statistics
+    import time
 
     import torch
     import torch.distributed as dist
 
     from . import synthetic as S
 
+    extras = extras or {}
     rank, world = init_process_group_from_env("nccl")
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     cfg = S.CONFIGS[args.config]
     data = S.corpus(cfg)  # deterministic on every rank; each keeps its shard
     shard, off = shard_corpus(data, rank, world)
+    seeds = S.init_seeds(data.n_docs, cfg.k, 0)
     gs = GPUShard(shard, off, data.n_docs, cfg.k, device=local, mode=args.mode, conv_sq_dist=1e-300,
                   max_iters=10 ** 6)
     comm = Comm(rank, world, torch.device("cuda", local))
     km = DistributedKMeans(gs, comm, data.n_docs, cfg.k, mode=args.mode)
-    km.init_from_seeds(S.init_seeds(data.n_docs, cfg.k, 0))
+    km.init_from_seeds(seeds)
     for _ in range(max(args.warmup, 3)):
         km.step()
     dist.barrier()
     torch.cuda.synchronize()
     gs.eng.synchronize()
+    clock = extras["clock"](local) if "clock" in extras else None
+    if clock:
+        clock.__enter__()
     gs.eng.timer_record(0)
     l0 = gs.eng.launch_count()
     stats = [km.step() for _ in range(args.steps)]
     gs.eng.timer_record(1)
     ms = gs.eng.timer_elapsed(0, 1)
+    if clock:
+        clock.__exit__(None, None, None)
     dist.barrier()
     ms_max = comm.all_reduce_f64_max(ms)
     launches = gs.eng.launch_count() - l0
     K = args.steps
+    e2e = None
+    if not getattr(args, "no_e2e", False):
+        del km, gs  # the timed engine's device memory goes back before the e2e engine is built
+        import gc
+
+        gc.collect()
+        # end to end through the shard API from host CSR: upload, seeding, K steps, download
+        dist.barrier()
+        t0 = time.perf_counter()
+        gs2 = GPUShard(shard, off, data.n_docs, cfg.k, device=local, mode=args.mode, conv_sq_dist=1e-300,
+                       max_iters=10 ** 6)
+        km2 = DistributedKMeans(gs2, comm, data.n_docs, cfg.k, mode=args.mode)
+        km2.init_from_seeds(seeds)
+        for _ in range(K):
+            km2.step()
+        a2, s2, _ = gs2.get_state()
+        wall = comm.all_reduce_f64_max(time.perf_counter() - t0)
+        h2d = shard.indptr.nbytes + shard.indices.nbytes + shard.values.nbytes + 4 * cfg.k
+        e2e = {"value": data.n_docs * cfg.k * K / wall, "unit": "comparisons/s",
+               "h2d_bytes_per_step": h2d * world / K, "d2h_bytes_per_step": (a2.nbytes + s2.nbytes) * world / K,
+               "wall_s": wall, "iterations": K,
+               "note": "every rank: shard upload, seeding, K steps, download of its assignments and sims; "
+                       "wall clock, max over ranks; bytes summed over ranks, amortised per step"}
+        del km2, gs2
     if rank == 0:
-        print(json.dumps({
+        line = {
             "metric": "effective doc·centroid comparisons/s", "value": data.n_docs * cfg.k * K / (ms_max / 1e3),
             "unit": "comparisons/s", "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3),
             "ms_per_step": ms_max / K, "s_per_iteration": ms_max / K / 1e3, "higher_is_better": True,
@@ -400,9 +486,17 @@ def bench_distributed(args):
                        "parallelism": f"doc-sharded x{world}, delta all-gather (NCCL)",
                        "l2": "inputs larger than L2"},
             "phase_ms": {"update": statistics.mean(s.update_ms for s in stats),
-                         "assign": statistics.mean(s.assign_ms for s in stats)},
+                         "assign": statistics.mean(s.assign_ms for s in stats),
+                         "screen": statistics.mean(s.screen_ms for s in stats)},
             "moved_per_iter": statistics.mean(s.n_moved for s in stats),
             "gpu_launches": launches,
-        }), flush=True)
+        }
+        if "roofline" in extras:
+            line["roofline"] = extras["roofline"](stats, data)
+        if clock:
+            line["clocks"] = clock.summary()
+        if e2e:
+            line["e2e"] = e2e
+        print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
