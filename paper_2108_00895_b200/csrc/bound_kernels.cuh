@@ -78,7 +78,7 @@ struct BoundArgs {
 // Per-warp shared memory of the bound screen (bytes).
 template <int KT>
 struct BoundSmem {
-    static constexpr int kCap = KT / 4;  // touched clusters tracked before a dense sweep
+    static constexpr int kCap = 256;  // touched clusters tracked before a dense sweep of the tile
     static constexpr uint32_t o_acc = 0;                   // int32[KT] fixed-point accumulators
     static constexpr uint32_t o_fold = o_acc + KT * 4;     // double[32] fold buffer
     static constexpr uint32_t o_tl = o_fold + 32 * 8;      // u16[kCap] touched list

@@ -1378,12 +1378,26 @@ private:
 
     template <typename K>
     void bound_launch_k(K k, size_t per_warp, const BoundArgs& p) {
-        const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (100u << 10) / per_warp)));
+        // warps per block: the most resident warps per SM (shared memory bounds
+        // the 2048-cluster tiles, registers the 1024-cluster ones)
+        int warps = 1, per_sm = 1, best = 0;
+        for (int w : {8, 4, 2}) {
+            const size_t sm = static_cast<size_t>(w) * per_warp;
+            if (sm > (200u << 10)) continue;
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+            int b = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, w * 32, sm));
+            if (b * w > best) {
+                best = b * w;
+                warps = w;
+                per_sm = std::max(1, b);
+            }
+        }
         const size_t smem = static_cast<size_t>(warps) * per_warp;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem));
-        per_sm = std::max(1, per_sm);
+        if (debug_)
+            std::fprintf(stderr, "[sskm] bound launch: %d warps/block, %d blocks/SM, %zu B smem/block\n", warps, per_sm,
+                         smem);
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
             1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(p.n_work, warps))));
         k<<<grid, warps * 32, smem, stream_>>>(p);
