@@ -58,6 +58,7 @@ struct BoundArgs {
     uint32_t k;
     int first;                 // first tile: establish the baseline and decide take
     int single_tile;           // the tile holds every column (its low maxima bound every cluster)
+    const unsigned long long* hp_overflow;  // the postings build dropped lists (then only Σ|x|·L_t bounds)
     uint32_t* a;               // in/out: running exact argmax
     double* sims;              // in/out: running exact max
     const uint8_t* unchanged;  // NCC: cached own similarity valid
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     const uint32_t w0 = blockIdx.x * chunk;
     const uint32_t w1 = min(n_work, w0 + chunk);
     const bool first = p.first != 0;
+    const bool hp_ovf = *p.hp_overflow != 0;
     const uint32_t* __restrict__ indptr = reinterpret_cast<const uint32_t*>(p.indptr32);
     auto doc_of = [&](uint32_t ww) -> uint32_t { return p.order ? __ldg(p.order + ww) : ww; };
     auto start_of = [&](uint32_t i) -> uint32_t {
@@ -391,6 +393,8 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         for (int off = 16; off > 0; off >>= 1) low += __shfl_xor_sync(0xFFFFFFFFu, low, off);
         low = low * (1.0 + (nn / 32.0 + 2.0) * 0x1p-23) * (1.0 + 1e-12);
         const double theta_x1 = p.theta * xb.x * (1.0 + 1e-12);
+        // θ·‖x‖₁ bounds only weights below θ: not valid once lists were dropped
+        const double lowb = hp_ovf ? low : fmin(low, theta_x1);
         if (first && active) {
             if (need_dot) {
                 best = s_own;
@@ -398,7 +402,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             }
             // no cluster without a high entry shared with x can exceed lb
             // (the tile's low maxima bound the clusters of this tile only)
-            const double lb = (p.single_tile ? fmin(low, theta_x1) : theta_x1) + g64 * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
+            const double lb = (p.single_tile ? lowb : theta_x1) + g64 * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
             const bool take = best > lb && (INIT != kInitFull || arg < p.k);
             if (lane == 0) {
                 p.take[w] = take ? 1 : 0;
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             // best, gathered 32 at a time (one per lane) and evaluated in
             // descending bound order, so the likely winner raises `best` first
             // and prunes the rest (a bound below best cannot win or tie)
-            const double bx = fmin(low, theta_x1) + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
+            const double bx = lowb + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
             // no touched cluster can reach best: nothing to evaluate
             const uint32_t count = static_cast<double>(accmax) * kFixUnit + bx >= best ? (dense ? p.kt : ntouch) : 0u;
             uint32_t c_gid = 0;   // this lane's pending candidate
@@ -523,7 +527,8 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
 __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
                                                            uint32_t c0, uint32_t kt, float thr,
                                                            uint4* __restrict__ hptr, uint2* __restrict__ pairs,
-                                                           unsigned long long cap, unsigned long long* total) {
+                                                           unsigned long long cap, unsigned long long* total,
+                                                           unsigned long long* overflow) {
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x / kWarp;
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
         const uint64_t t = tb + warp;
         const float* row = M + t * ld + c0;
         uint32_t cnt = 0;
-        float lowmax = 0.f;
+        float lowmax = 0.f, allmax = 0.f;
         if (t < d) {
             // 16-byte loads over the row (tiles start at multiples of 4 columns)
             const uint32_t kt4 = kt & ~3u;
@@ -544,18 +549,21 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
                     const bool k = post_keep(e[r], thr);
                     cnt += k;
                     lowmax = k ? lowmax : fmaxf(lowmax, fabsf(e[r]));
+                    allmax = fmaxf(allmax, fabsf(e[r]));
                 }
             }
             for (uint32_t j = kt4 + lane; j < kt; j += kWarp) {
                 const bool k = post_keep(row[j], thr);
                 cnt += k;
                 lowmax = k ? lowmax : fmaxf(lowmax, fabsf(row[j]));
+                allmax = fmaxf(allmax, fabsf(row[j]));
             }
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
             lowmax = fmaxf(lowmax, __shfl_xor_sync(0xFFFFFFFFu, lowmax, off));
+            allmax = fmaxf(allmax, __shfl_xor_sync(0xFFFFFFFFu, allmax, off));
         }
         if (lane == 0) s_cnt[warp] = cnt;
         __syncthreads();
@@ -569,8 +577,16 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
         unsigned long long b = s_base;
         for (int q = 0; q < warp; ++q) b += s_cnt[q];
         if (t < d) {
-            if (lane == 0) hptr[t] = make_uint4(static_cast<uint32_t>(b), cnt, __float_as_uint(lowmax), 0u);
-            if (cnt > 0 && b + cnt <= cap) {
+            // a list past the buffer's end is dropped, and the term's bound then
+            // covers every weight of the row (count 0, L_t = max |value|): the
+            // screen stays exact, only looser (the host grows the buffer after)
+            const bool fits = b + cnt <= cap;
+            if (lane == 0) {
+                hptr[t] = fits ? make_uint4(static_cast<uint32_t>(b), cnt, __float_as_uint(lowmax), 0u)
+                               : make_uint4(0u, 0u, __float_as_uint(allmax), 0u);
+                if (!fits) atomicOr(overflow, 1ull);
+            }
+            if (cnt > 0 && fits) {
                 uint32_t run = 0;
                 for (uint32_t j0 = 0; j0 < kt; j0 += kWarp) {
                     const uint32_t j = j0 + lane;

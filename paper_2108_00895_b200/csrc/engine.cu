@@ -973,7 +973,10 @@ private:
         sort_tmp_.alloc(std::max(t1, t2));
         scan_tmp_.alloc(t3);
         // postings: start at 10% density of a 2048-cluster tile, grow by 1.5x
-        pairs_.alloc(std::max<size_t>(1, static_cast<size_t>(d_) * std::min<uint32_t>(ld_, 2048) / 10));
+        // (SSKM_PAIRS_CAP: a smaller start, to exercise the overflow path)
+        size_t cap0 = std::max<size_t>(1, static_cast<size_t>(d_) * std::min<uint32_t>(ld_, 2048) / 10);
+        if (const char* e = std::getenv("SSKM_PAIRS_CAP")) cap0 = std::max<size_t>(1, std::strtoull(e, nullptr, 10));
+        pairs_.alloc(cap0);
     }
 
     // Bound on the centroid column norms after a seed init (the screen's δ).
@@ -1286,7 +1289,7 @@ private:
         for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
             const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
             if (c0 > 0) CK(cudaEventRecord(ev_[8], stream_));
-            build_hipost(M, ld, c0, kt, thr);  // synchronises (capacity check)
+            build_hipost(M, ld, c0, kt, thr, ncols > KT);  // multi-tile: synchronises (capacity check)
             if (c0 > 0) {
                 CK(cudaEventRecord(ev_[9], stream_));
                 CK(cudaEventSynchronize(ev_[9]));
@@ -1300,6 +1303,7 @@ private:
             p.kt = kt;
             p.first = c0 == 0 ? 1 : 0;
             p.single_tile = ncols <= KT ? 1 : 0;
+            p.hp_overflow = hpctr_.p + 1;
             // the screen launches are timed as one interval: the event pair
             // brackets every tile's screen, and the postings builds between
             // tiles are timed separately (build_ms) and subtracted
@@ -1316,11 +1320,14 @@ private:
                    sims_start_.p, sims_.p, unchanged_.p, rescan_.p, &scal_.p->n_rescan);
         // θ for the next assign: keep the exact-scan share small and the
         // candidate dots near one per document (θ never changes a result)
-        unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
+        unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0}, hp[2] = {0, 0};
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(hp, hpctr_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
         scalars_fresh_ = true;
+        if (hp[0] > pairs_.n) grow_pairs(hp[0]);  // the last tile's lists overflowed: room for the next pass
+        last_hp_overflow_ = hp[1] != 0;
         const uint64_t n_fb = hs_->n_exact;
         {
             float ms = 0.f;
@@ -1379,7 +1386,22 @@ private:
     template <typename K>
     void bound_launch_k(K k, size_t per_warp, const BoundArgs& p) {
         // warps per block: the most resident warps per SM (shared memory bounds
-        // the 2048-cluster tiles, registers the 1024-cluster ones)
+        // the 2048-cluster tiles, registers the 1024-cluster ones); chosen once
+        // per kernel
+        const void* key = reinterpret_cast<const void*>(k);
+        auto it = launch_cfg_.find(key);
+        if (it == launch_cfg_.end()) it = launch_cfg_.emplace(key, pick_bound_cfg(k, per_warp)).first;
+        const int warps = it->second.first, per_sm = it->second.second;
+        const size_t smem = static_cast<size_t>(warps) * per_warp;
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(p.n_work, warps))));
+        k<<<grid, warps * 32, smem, stream_>>>(p);
+        ++launches_;
+        CK_LAUNCH();
+    }
+
+    template <typename K>
+    std::pair<int, int> pick_bound_cfg(K k, size_t per_warp) {
         int warps = 1, per_sm = 1, best = 0;
         for (int w : {8, 4, 2}) {
             const size_t sm = static_cast<size_t>(w) * per_warp;
@@ -1398,32 +1420,38 @@ private:
         if (debug_)
             std::fprintf(stderr, "[sskm] bound launch: %d warps/block, %d blocks/SM, %zu B smem/block\n", warps, per_sm,
                          smem);
-        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-            1, std::min<int64_t>(static_cast<int64_t>(sms_) * per_sm, ceil_div(p.n_work, warps))));
-        k<<<grid, warps * 32, smem, stream_>>>(p);
-        ++launches_;
-        CK_LAUNCH();
+        return {warps, per_sm};
     }
 
     // High postings (|value| >= thr) of the columns [c0, c0 + kt) of M into
     // hptr_ / pairs_ in one pass over M; grows the pair buffer and rebuilds
     // when the previous capacity was exceeded.
-    void build_hipost(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr) {
+    // High postings of the tile [c0, c0 + kt) of M. With `check`, wait for the
+    // pair count and rebuild in a grown buffer when it overflowed (multi-tile
+    // passes, whose first tile bounds the later tiles' clusters by θ·‖x‖₁);
+    // without, an overflow only loosens the bound (the dropped lists' weights
+    // are covered by L_t) and the host grows the buffer after the pass.
+    void build_hipost(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr, bool check) {
         hptr_.alloc(d_);
-        hpctr_.alloc(1);
+        hpctr_.alloc(2);
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 8));
         for (int attempt = 0; attempt < 2; ++attempt) {
-            CK(cudaMemsetAsync(hpctr_.p, 0, sizeof(unsigned long long), stream_));
+            CK(cudaMemsetAsync(hpctr_.p, 0, 2 * sizeof(unsigned long long), stream_));
             launch(hipost_build_kernel, grid, 256, M, ld, d_, c0, kt, thr, hptr_.p, pairs_.p,
-                   static_cast<unsigned long long>(pairs_.n), hpctr_.p);
+                   static_cast<unsigned long long>(pairs_.n), hpctr_.p, hpctr_.p + 1);
             CK_LAUNCH();
+            if (!check) return;
             unsigned long long total = 0;
             CK(cudaMemcpyAsync(&total, hpctr_.p, 8, cudaMemcpyDeviceToHost, stream_));
             CK(cudaStreamSynchronize(stream_));
             if (total <= pairs_.n) return;
-            if (total >= (1ull << 32)) throw std::runtime_error("bound screen: high postings exceed 2^32 pairs");
-            pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
+            grow_pairs(total);
         }
+    }
+
+    void grow_pairs(unsigned long long total) {
+        if (total >= (1ull << 32)) throw std::runtime_error("bound screen: high postings exceed 2^32 pairs");
+        pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
     }
 
     bool screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
@@ -1794,7 +1822,9 @@ private:
     uint32_t post_kt_max_ = 1024;
     int post_warps_ = 8;
     bool cache_trusted_ = false;
-    bool scalars_fresh_ = false;  // hs_ was pulled by the last bound-screen pass
+    bool scalars_fresh_ = false;
+    std::map<const void*, std::pair<int, int>> launch_cfg_;  // bound screen: (warps per block, blocks per SM)
+    bool last_hp_overflow_ = false;  // the last pass ran with dropped postings lists (looser bound)  // hs_ was pulled by the last bound-screen pass
     bool fuse_resolve_ = false;
     bool bound_enabled_ = true;   // bound screen (SSKM_BOUND=0: the full postings / dense screens)
     bool theta_adapt_ = true;

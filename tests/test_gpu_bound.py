@@ -99,3 +99,16 @@ def test_bound_default_teacher_forced_against_oracle():
         ra, rs, _ = ref.get_state()
         assert np.array_equal(ra, a), it
         assert np.array_equal(rs, s), it
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_postings_overflow_stays_exact(case, monkeypatch):
+    """A high-postings buffer too small for the first bound pass: single-tile
+    passes drop the overflowing lists and bound those terms by their largest
+    weight (looser, still exact); multi-tile passes grow and rebuild."""
+    m, k = CASES[case]()
+    seeds = np.random.default_rng(0).choice(m.n_docs, k, replace=False)
+    ref, _ = trajectory(m, k, seeds, "baseline", 4)
+    monkeypatch.setenv("SSKM_PAIRS_CAP", "64")
+    t, _ = trajectory(m, k, seeds, "baseline", 4)
+    assert_same(ref, t, "pairs cap 64")
