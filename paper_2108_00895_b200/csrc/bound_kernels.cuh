@@ -337,8 +337,9 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, kWarp - 1);
                 const uint32_t adj = ext.x - (incl - cnt);  // pair index = adj + slot
                 const float xs = x * kFixScale;
-                for (uint32_t wb = 0; wb < total; wb += kWarp) {
-                    const uint32_t sl = wb + lane;
+                // two windows per round: both windows' pair loads are in flight
+                // before either window's accumulator updates
+                auto slot = [&](uint32_t sl, uint2& pr, float& xq) {
                     int lo = 0;
 #pragma unroll
                     for (int step = 16; step > 0; step >>= 1) {
@@ -346,21 +347,29 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                         if (v <= sl) lo += step;
                     }
                     const uint32_t base_o = __shfl_sync(0xFFFFFFFFu, adj, lo & (kWarp - 1));
-                    const float xs_o = __shfl_sync(0xFFFFFFFFu, xs, lo & (kWarp - 1));
-                    if (sl < total) {
-                        const uint2 pr = ld_pair(pairs + (base_o + sl), pol_keep);
-                        if (pr.x != own_l) {
-                            const int qv = __float2int_rn(xs_o * __uint_as_float(pr.y));
-                            if (qv != 0) {
-                                const int old = sm_atom_add(s_acc + 4u * pr.x, qv);
-                                accmax = max(accmax, old + qv);  // every final value is some old + qv
-                                if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
-                                    const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
-                                    if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr.x);
-                                }
+                    xq = __shfl_sync(0xFFFFFFFFu, xs, lo & (kWarp - 1));
+                    pr = sl < total ? ld_pair(pairs + (base_o + sl), pol_keep) : make_uint2(kNone, 0u);
+                };
+                auto accumulate = [&](const uint2 pr, const float xq) {
+                    if (pr.x != kNone && pr.x != own_l) {
+                        const int qv = __float2int_rn(xq * __uint_as_float(pr.y));
+                        if (qv != 0) {
+                            const int old = sm_atom_add(s_acc + 4u * pr.x, qv);
+                            accmax = max(accmax, old + qv);  // every final value is some old + qv
+                            if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
+                                const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
+                                if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr.x);
                             }
                         }
                     }
+                };
+                for (uint32_t wb = 0; wb < total; wb += 2 * kWarp) {
+                    uint2 pa, pb;
+                    float xa, xb2;
+                    slot(wb + lane, pa, xa);
+                    slot(wb + kWarp + lane, pb, xb2);
+                    accumulate(pa, xa);
+                    accumulate(pb, xb2);
                 }
                 // the next chunk's extents, now that its terms have arrived: in
                 // flight during this chunk's fold and the loop turn
