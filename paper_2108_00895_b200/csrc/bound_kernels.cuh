@@ -596,15 +596,37 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
                 if (!fits) atomicOr(overflow, 1ull);
             }
             if (cnt > 0 && fits) {
+                // 16-byte loads again (the row is in L1/L2 now); each lane's kept
+                // values go to its prefix position within the 128 columns
                 uint32_t run = 0;
-                for (uint32_t j0 = 0; j0 < kt; j0 += kWarp) {
+                const uint32_t kt4 = kt & ~3u;
+                for (uint32_t j0 = 0; j0 < kt4 && run < cnt; j0 += 4u * kWarp) {
+                    const uint32_t j = j0 + 4u * lane;
+                    float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (j < kt4) v4 = __ldg(reinterpret_cast<const float4*>(row + j));
+                    const float e[4] = {v4.x, v4.y, v4.z, v4.w};
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) mine += post_keep(e[r], thr);
+                    uint32_t incl = mine;
+#pragma unroll
+                    for (int off = 1; off < kWarp; off <<= 1) {
+                        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+                        if (lane >= off) incl += o;
+                    }
+                    uint64_t o = b + run + (incl - mine);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (post_keep(e[r], thr)) pairs[o++] = make_uint2(j + r, __float_as_uint(e[r]));
+                    run += __shfl_sync(0xFFFFFFFFu, incl, kWarp - 1);
+                }
+                for (uint32_t j0 = kt4; j0 < kt && run < cnt; j0 += kWarp) {  // the tail columns
                     const uint32_t j = j0 + lane;
                     const float v = j < kt ? row[j] : 0.f;
                     const bool keep = j < kt && post_keep(v, thr);
                     const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
                     if (keep) pairs[b + run + __popc(m & lt)] = make_uint2(j, __float_as_uint(v));
                     run += __popc(m);
-                    if (run == cnt) break;
                 }
             }
         }

@@ -1010,7 +1010,11 @@ private:
     void local_counts_device() {
         CK(cudaMemsetAsync(counts_.p, 0, k_ * 8, stream_));
         reset_scalars();
-        launch(counts_kernel, grid_for(n_, 256), 256, a_.p, n_, k_, counts_.p, &scal_.p->bad);
+        if (k_ <= kSmemBins)
+            launch(counts_smem_kernel, static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(sms_, ceil_div(n_, 1024)))),
+                   1024, a_.p, n_, k_, counts_.p, &scal_.p->bad);
+        else
+            launch(counts_kernel, grid_for(n_, 256), 256, a_.p, n_, k_, counts_.p, &scal_.p->bad);
         CK_LAUNCH();
     }
 

@@ -24,6 +24,28 @@
 
 namespace sskm_b200 {
 
+// Cluster sizes through a per-block shared histogram (k ≤ kSmemBins): one
+// global atomic per nonzero bin and block instead of one per document.
+constexpr uint32_t kSmemBins = 8192;
+__global__ void __launch_bounds__(1024) counts_smem_kernel(const uint32_t* __restrict__ a, int64_t n, uint32_t k,
+                                                           unsigned long long* __restrict__ counts, unsigned int* bad) {
+    __shared__ unsigned int h[kSmemBins];
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) h[j] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t c = a[i];
+        if (c >= k) {
+            atomicOr(bad, 1u);
+            continue;
+        }
+        atomicAdd(h + c, 1u);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x)
+        if (h[j]) atomicAdd(counts + j, static_cast<unsigned long long>(h[j]));
+}
+
 __global__ void counts_kernel(const uint32_t* __restrict__ a, int64_t n, uint32_t k,
                               unsigned long long* __restrict__ counts, unsigned int* bad) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
