@@ -631,7 +631,10 @@ public:
     void full_assign(sskm_iteration_stats* st) {
         CK(cudaEventRecord(ev_[2], stream_));
         snapshot_start();
-        const uint32_t* order = cluster_order();
+        // the bound screen streams documents in index order (consecutive CSR rows:
+        // measured 1.75 -> 1.40 ms per c1 screen against the cluster order the
+        // tile scans prefer)
+        const uint32_t* order = bound_active() ? nullptr : cluster_order();
         reset_scalars();
         CK(cudaEventRecord(ev_[4], stream_));
         uint64_t n_exact = 0;
@@ -659,7 +662,10 @@ public:
         CK(cudaEventRecord(ev_[2], stream_));
         snapshot_start();
         ensure_cc();
-        const uint32_t* order = cluster_order();
+        // the bound screen streams documents in index order (consecutive CSR rows:
+        // measured 1.75 -> 1.40 ms per c1 screen against the cluster order the
+        // tile scans prefer)
+        const uint32_t* order = bound_active() ? nullptr : cluster_order();
         reset_scalars();
         CK(cudaEventRecord(ev_[4], stream_));
         uint64_t n_exact = 0, n_rescan = 0;
@@ -1458,11 +1464,13 @@ private:
         pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
     }
 
+    bool bound_active() const { return screen_enabled_ && bound_enabled_ && bound_ok_ && iteration_ >= 1; }
+
     bool screen_any(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
                     const uint32_t* order, int64_t n_work, int init) {
         // the bound screen needs a real assignment to start from: not the
         // seed assignment (iteration 0), whose state is all cluster 0
-        if (bound_enabled_ && bound_ok_ && iteration_ >= 1) {
+        if (bound_active()) {
             bound_assign(M, ld, ncols, col_ids, order, n_work, init);
             return true;  // candidates resolved exactly in the kernel; the exact list holds the rest
         }
