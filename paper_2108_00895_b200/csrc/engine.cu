@@ -263,6 +263,10 @@ public:
     // -------------------------------------------------------------- init --
     void reset_sums() {
         CK(cudaMemsetAsync(S_.p, 0, static_cast<uint64_t>(d_) * ld_ * sizeof(long long), stream_));
+        // every group marked: Cᵀ may hold values the fresh sums do not (seeds,
+        // teacher forcing); the first rewrite clears the marks of empty groups
+        nz_.alloc(static_cast<size_t>(d_) * (ld_ / 32));
+        CK(cudaMemsetAsync(nz_.p, 0xFF, static_cast<size_t>(d_) * (ld_ / 32) * sizeof(unsigned int), stream_));
         CK(cudaMemsetAsync(Q_.p, 0, 2 * static_cast<size_t>(k_) * sizeof(unsigned long long), stream_));
         launch(fill_u32_kernel, grid_for(n_, 256), 256, a_sum_.p, n_, kNone);
         CK_LAUNCH();
@@ -386,7 +390,7 @@ public:
         CK_LAUNCH();
         launch(delta_local_kernel, grid_for(n_ * 32, 256), 256, 
             indptr_.p, idx_.p, val_.p, moved_.p, &scal_.p->n_moved, a_.p, a_sum_.p, S_.p, ld_, K_,
-            touched_.p, Q_.p);
+            touched_.p, Q_.p, nz_.p);
         CK_LAUNCH();
         finish_update(st);
         float ms = 0.f;
@@ -413,7 +417,7 @@ public:
         reset_scalars();
         if (n_moved > 0) {
             launch(delta_packed_kernel, grid_for(n_moved * 32, 256), 256, 
-                n_moved, old_c, new_c, row_ptr, idx, val, S_.p, ld_, K_, touched_.p, Q_.p);
+                n_moved, old_c, new_c, row_ptr, idx, val, S_.p, ld_, K_, touched_.p, Q_.p, nz_.p);
             CK_LAUNCH();
         }
         finish_update(st);
@@ -1124,7 +1128,7 @@ private:
             launch(q_norm2_kernel, static_cast<unsigned>(ceil_div(k_, 128)), 128, Q_.p, rec_ids_.p, n_rec_dev,
                    norm2_.p);
             launch(write_cols_kernel, grid, 128, S_.p, ct_.p, ld_, d_, rec_ids_.p, n_rec_dev, k_, norm2_.p, part_.p,
-                   &scal_.p->zero_flag);
+                   &scal_.p->zero_flag, nz_.p);
             launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 256, part_.p, n_rb, n_rec_dev, k_,
                    drift_rec_.p);
             launch(scatter_pos_dev_kernel, grid_for(k_, 256), 256, rec_ids_.p, n_rec_dev, rec_pos_.p);
@@ -1862,6 +1866,7 @@ private:
     DevBuf<uint32_t> order_, keys32_;
     DevBuf<double> sims_, drift_, norm2_, drift_rec_, part_, obj_part_;
     DevBuf<unsigned long long> Q_;  // exact Σ_t S[t][j]² per column (128-bit: lo, hi)
+    DevBuf<unsigned int> nz_;       // a bit per (term, cluster): S or Cᵀ may be nonzero there
     DevBuf<uint8_t> unchanged_, touched_, repaired_flag_;
     DevBuf<unsigned long long> counts_, keys_;
     DevBuf<uint32_t> vals_, moves_, mv_old_, mv_new_;

@@ -82,10 +82,18 @@ __device__ __forceinline__ long long quantize(float x, int K) {
     return __double2ll_rn(ldexp(static_cast<double>(x), K));
 }
 
-// S[row + c] += q; returns q·(2·old + q), the exact change of Σ S² (128-bit).
-__device__ __forceinline__ __int128 add_sum(long long* S, uint64_t o, long long q) {
+// S[t·ld + c] += q; returns q·(2·old + q), the exact change of Σ S² (128-bit).
+// A nonzero result marks (t, c) in the bitmap nz (ld/32 words per row): the
+// column rewrite reads only marked entries, and unmarks the ones it zeroes.
+__device__ __forceinline__ __int128 add_sum(long long* S, uint64_t t, uint64_t ld, uint32_t c, long long q,
+                                            unsigned int* nz) {
     const long long old = static_cast<long long>(
-        atomicAdd(reinterpret_cast<unsigned long long*>(S + o), static_cast<unsigned long long>(q)));
+        atomicAdd(reinterpret_cast<unsigned long long*>(S + t * ld + c), static_cast<unsigned long long>(q)));
+    if (old + q != 0) {
+        unsigned int* w = nz + t * (ld >> 5) + (c >> 5);
+        const unsigned int bit = 1u << (c & 31u);
+        if (!(*w & bit)) atomicOr(w, bit);
+    }
     return static_cast<__int128>(q) * (2 * static_cast<__int128>(old) + q);
 }
 
@@ -116,7 +124,7 @@ __global__ void delta_local_kernel(const int64_t* __restrict__ indptr, const int
                                    const unsigned long long* n_moved_p, const uint32_t* __restrict__ a,
                                    uint32_t* __restrict__ a_sum, long long* __restrict__ S,
                                    uint64_t ld, int K, uint8_t* __restrict__ touched,
-                                   unsigned long long* __restrict__ Q) {
+                                   unsigned long long* __restrict__ Q, unsigned int* __restrict__ nz) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
@@ -128,9 +136,9 @@ __global__ void delta_local_kernel(const int64_t* __restrict__ indptr, const int
         __int128 dn = 0, dold = 0;
         for (int64_t e = beg + lane; e < end; e += kWarp) {
             const long long q = quantize(val[e], K);
-            const uint64_t row = static_cast<uint64_t>(idx[e]) * ld;
-            dn += add_sum(S, row + nc, q);
-            if (oc != kNone) dold += add_sum(S, row + oc, -q);
+            const uint64_t t = static_cast<uint64_t>(idx[e]);
+            dn += add_sum(S, t, ld, nc, q, nz);
+            if (oc != kNone) dold += add_sum(S, t, ld, oc, -q, nz);
         }
         dn = warp_sum128(dn);
         if (oc != kNone) dold = warp_sum128(dold);
@@ -152,7 +160,8 @@ __global__ void delta_packed_kernel(int64_t n_moved, const uint32_t* __restrict_
                                     const int64_t* __restrict__ row_ptr,
                                     const int32_t* __restrict__ idx, const float* __restrict__ val,
                                     long long* __restrict__ S, uint64_t ld, int K,
-                                    uint8_t* __restrict__ touched, unsigned long long* __restrict__ Q) {
+                                    uint8_t* __restrict__ touched, unsigned long long* __restrict__ Q,
+                                    unsigned int* __restrict__ nz) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
@@ -161,9 +170,9 @@ __global__ void delta_packed_kernel(int64_t n_moved, const uint32_t* __restrict_
         __int128 dn = 0, dold = 0;
         for (int64_t e = row_ptr[m] + lane; e < row_ptr[m + 1]; e += kWarp) {
             const long long q = quantize(val[e], K);
-            const uint64_t row = static_cast<uint64_t>(idx[e]) * ld;
-            dn += add_sum(S, row + nc, q);
-            if (oc != kNone) dold += add_sum(S, row + oc, -q);
+            const uint64_t t = static_cast<uint64_t>(idx[e]);
+            dn += add_sum(S, t, ld, nc, q, nz);
+            if (oc != kNone) dold += add_sum(S, t, ld, oc, -q, nz);
         }
         dn = warp_sum128(dn);
         if (oc != kNone) dold = warp_sum128(dold);
@@ -304,7 +313,7 @@ __global__ void write_cols_kernel(const long long* __restrict__ S, float* __rest
                                   uint64_t ld, uint32_t d, const uint32_t* __restrict__ ids,
                                   const unsigned int* __restrict__ n_dev, uint32_t stride,
                                   const double* __restrict__ norm2, double* __restrict__ part,
-                                  unsigned int* zero_flag) {
+                                  unsigned int* zero_flag, unsigned int* __restrict__ nz) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t rb = blockIdx.y;
     if (c >= *n_dev) return;
@@ -316,6 +325,10 @@ __global__ void write_cols_kernel(const long long* __restrict__ S, float* __rest
     }
     const double inv = 1.0 / nrm;
     const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
+    // unmarked (t, j) have S = 0 and Cᵀ = 0: nothing to read or write (the marks
+    // are a superset: set by the delta kernels, cleared here once an entry is 0)
+    const uint64_t wpr = ld >> 5;
+    const uint32_t gw = j >> 5, gb = 1u << (j & 31u);
     double dr = 0.0;
     // 8 rows per step, all loads issued before any store (the compiler cannot
     // prove the Cᵀ store of one row does not alias the next row's load)
@@ -323,11 +336,14 @@ __global__ void write_cols_kernel(const long long* __restrict__ S, float* __rest
     for (uint32_t tb = t0; tb < t1; tb += kB) {
         long long q[kB];
         float old[kB];
+        bool on[kB];
+#pragma unroll
+        for (int r = 0; r < kB; ++r) on[r] = tb + r < t1 && (nz[static_cast<uint64_t>(tb + r) * wpr + gw] & gb);
 #pragma unroll
         for (int r = 0; r < kB; ++r) {
             const uint64_t o = static_cast<uint64_t>(tb + r) * ld + j;
-            q[r] = tb + r < t1 ? __ldcs(S + o) : 0;
-            old[r] = tb + r < t1 ? CT[o] : 0.f;
+            q[r] = on[r] ? __ldcs(S + o) : 0;
+            old[r] = on[r] ? CT[o] : 0.f;
         }
 #pragma unroll
         for (int r = 0; r < kB; ++r) {
@@ -335,6 +351,7 @@ __global__ void write_cols_kernel(const long long* __restrict__ S, float* __rest
             const double diff = static_cast<double>(cn) - static_cast<double>(old[r]);
             dr = fma(diff, diff, dr);
             if (cn != old[r]) CT[static_cast<uint64_t>(tb + r) * ld + j] = cn;
+            if (on[r] && q[r] == 0) atomicAnd(nz + static_cast<uint64_t>(tb + r) * wpr + gw, ~gb);
         }
     }
     part[static_cast<uint64_t>(rb) * stride + c] = dr;
