@@ -75,12 +75,12 @@ typedef struct {
     uint32_t n_changed;       /* centroids scanned by the NCC pass (unchanged flag clear) */
     uint32_t n_recomputed;    /* centroid columns rewritten by the update */
     uint64_t n_rescan;        /* NCC documents that needed the unchanged-centroid pass */
-    uint64_t n_exact;         /* documents the fp32 screen could not certify (exact fp64 scan) */
+    uint64_t n_exact;         /* documents the screen handed to the exact fp64 tile scan */
     double update_ms;         /* device time of compute_centroids + detect_unchanged */
     double assign_ms;         /* device time of the assignment step */
     double assign_kernel_ms;  /* device time of the assign kernels (screen, resolve, exact) */
-    double screen_ms;         /* device time of the postings-screen kernel launches only */
-    uint32_t screen_launches; /* postings-screen launches in this assign (one per cluster tile) */
+    double screen_ms;         /* device time of the screen kernel launches only (bound or postings screen) */
+    uint32_t screen_launches; /* screen launches in this assign (one per cluster tile) */
     uint32_t reserved0;
     double centroid_density;  /* nonzero fraction of the centroid tile last indexed (screen choice) */
     /* bound screen (the default screen after the seed assignment) */
