@@ -94,22 +94,6 @@ __device__ __forceinline__ uint32_t sm_ld_u32(uint32_t a) {
     return v;
 }
 __device__ __forceinline__ void sm_st_u32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
-__device__ __forceinline__ uint2 sm_ld_u64(uint32_t a) {
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sm_st_u64(uint32_t a, uint2 v) {
-    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(v.x), "r"(v.y));
-}
-__device__ __forceinline__ uint32_t sm_ld_u8(uint32_t a) {
-    uint16_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sm_st_u8(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)));
-}
 __device__ __forceinline__ uint32_t sm_ld_u16(uint32_t a) {
     uint16_t v;
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -123,11 +107,6 @@ __device__ __forceinline__ int sm_atom_add(uint32_t a, int v) {
     asm volatile("atom.shared.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
     return old;
 }
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Loads and a conversion as volatile asm: the compiler keeps them where they
 // are written (it otherwise converts a gathered weight right after its load,
