@@ -19,7 +19,7 @@ HEADER = os.path.join(os.path.dirname(PKG), "include", "sskm_b200.h")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O3",
+    "-Xcompiler", "-fPIC,-O3,-fopenmp", "-lgomp",
     "-Xptxas", "-v",
     "-shared", "-cudart", "static",
 ] + [f for f in os.environ.get("SSKM_NVCC_EXTRA", "").split() if f]
