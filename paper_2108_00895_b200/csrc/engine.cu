@@ -117,7 +117,7 @@ public:
         for (int b = 0; b < 2; ++b)
             if (stage_[b]) {
                 cudaFreeHost(stage_[b]);
-                cudaEventDestroy(stage_ev_[b]);
+                if (stage_ev_[b]) cudaEventDestroy(stage_ev_[b]);
             }
         for (auto& e : user_ev_) cudaEventDestroy(e);
         cudaStreamDestroy(stream_);
@@ -155,16 +155,21 @@ public:
     // other's DMA runs. The driver's own pageable path runs at ~8 GB/s here.
     void h2d(void* dst, const void* src, size_t bytes) {
         constexpr size_t kChunk = size_t(64) << 20;
-        if (bytes < (size_t(8) << 20)) {
-            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
-            return;
-        }
-        for (int b = 0; b < 2; ++b)
+        for (int b = 0; b < 2 && bytes >= (size_t(8) << 20) && !stage_failed_; ++b)
             if (!stage_[b]) {
-                CK(cudaMallocHost(&stage_[b], kChunk));
+                if (cudaMallocHost(&stage_[b], kChunk) != cudaSuccess) {  // no pinned memory: pageable copies
+                    (void)cudaGetLastError();
+                    stage_[b] = nullptr;
+                    stage_failed_ = true;
+                    break;
+                }
                 CK(cudaEventCreateWithFlags(&stage_ev_[b], cudaEventDisableTiming));
                 stage_used_[b] = false;
             }
+        if (bytes < (size_t(8) << 20) || stage_failed_) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
+            return;
+        }
         size_t off = 0;
         for (int i = 0; off < bytes; ++i, off += kChunk) {
             const int b = i & 1;
@@ -1890,7 +1895,8 @@ private:
     std::map<const void*, std::pair<int, int>> launch_cfg_;
     void* stage_[2] = {nullptr, nullptr};  // pinned upload staging (h2d)
     cudaEvent_t stage_ev_[2]{};
-    bool stage_used_[2] = {false, false};  // bound screen: (warps per block, blocks per SM)
+    bool stage_used_[2] = {false, false};
+    bool stage_failed_ = false;  // pinned staging unavailable: pageable copies  // bound screen: (warps per block, blocks per SM)
     bool last_hp_overflow_ = false;  // the last pass ran with dropped postings lists (looser bound)  // hs_ was pulled by the last bound-screen pass
     bool fuse_resolve_ = false;
     bool bound_enabled_ = true;   // bound screen (SSKM_BOUND=0: the full postings / dense screens)
