@@ -93,6 +93,8 @@ public:
             theta_ = static_cast<float>(std::atof(e));
             theta_adapt_ = false;
         }
+        if (const char* e = std::getenv("SSKM_THETA0"))  // starting point of the adaptive θ
+            for (auto& c : tctl_) c.theta = static_cast<float>(std::atof(e));
         if (const char* e = std::getenv("SSKM_POST_KT")) post_kt_max_ = static_cast<uint32_t>(std::atoi(e));
         if (const char* e = std::getenv("SSKM_POST_WARPS")) post_warps_ = std::max(1, std::min(8, std::atoi(e)));
         if (const char* e = std::getenv("SSKM_DENSE_ABOVE")) dense_above_ = std::atof(e);
