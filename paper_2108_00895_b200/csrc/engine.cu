@@ -1503,7 +1503,7 @@ private:
     void build_hipost(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr, bool check) {
         hptr_.alloc(d_);
         hpctr_.alloc(2);
-        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 8));
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 32));
         for (int attempt = 0; attempt < 2; ++attempt) {
             CK(cudaMemsetAsync(hpctr_.p, 0, 2 * sizeof(unsigned long long), stream_));
             launch(hipost_build_kernel, grid, 256, M, ld, d_, c0, kt, thr, hptr_.p, pairs_.p,
