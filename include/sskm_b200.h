@@ -55,7 +55,10 @@ typedef struct {
 /* IterationStats, engine.hpp:43-57, followed by GPU extras. `dot_products`
  * counts exactly what the reference's assign would have evaluated
  * (engine.cpp:253-306) so the reference's accounting invariants hold;
- * `gpu_dot_products` is what the kernels evaluated. */
+ * `gpu_dot_products` is what the kernels evaluated: full (document, centroid)
+ * dots — exact fp64 ones (bound-screen candidates and own-cluster dots, exact
+ * tile scans) and the fp32 screens' dots — not the bound screen's partial sums
+ * over high centroid entries. */
 typedef struct {
     uint32_t iteration;
     uint32_t n_unchanged_centroids;
@@ -149,13 +152,17 @@ int sskm_set_state(sskm_ctx* ctx, const uint32_t* assignments, const double* sim
 /* Centroids as Cᵀ, d rows × k columns, row-major fp32. */
 int sskm_get_centroids(sskm_ctx* ctx, float* ct);
 int sskm_set_centroids(sskm_ctx* ctx, const float* ct);
+/* Slices of Cᵀ for large-k checks (the dense d×k copy is 26 GB at config 4):
+ * rows[0..n_rows) of Cᵀ → out[n_rows][k]; columns cols[0..n_cols) → out[d][n_cols]. */
+int sskm_get_centroid_rows(sskm_ctx* ctx, uint32_t n_rows, const uint32_t* rows, float* out);
+int sskm_get_centroid_cols(sskm_ctx* ctx, uint32_t n_cols, const uint32_t* cols, float* out);
 /* Teacher forcing of the NCC flags (unchanged[j] = 1: cluster j skipped by the
  * changed-list scan); extension, no reference counterpart. */
 int sskm_set_unchanged(sskm_ctx* ctx, const uint8_t* unchanged);
 int sskm_get_repaired(sskm_ctx* ctx, uint32_t* repaired, uint32_t* n_repaired);
 int sskm_get_iteration(sskm_ctx* ctx, uint32_t* iteration);
 
-/* Device timing on the context's stream (CUDA events; 16 slots) and the
+/* Device timing on the context's stream (CUDA events; 256 slots) and the
  * number of kernels this context has launched — the bench's live evidence. */
 int sskm_timer_record(sskm_ctx* ctx, int32_t slot);
 int sskm_timer_elapsed(sskm_ctx* ctx, int32_t a, int32_t b, double* ms);

@@ -105,6 +105,11 @@ def _load(kind: str):
         lib.sref_stepper_new.argtypes = [_P, C.c_uint32, C.c_char_p, C.c_double, C.c_double,
                                          C.c_uint32, C.c_uint32, C.c_uint32]
         lib.sref_stepper_free.argtypes = [_P]
+        lib.sref_stepper_new_sample.restype = _P
+        lib.sref_stepper_new_sample.argtypes = [_P, C.c_uint32, C.c_char_p, C.c_double, C.c_uint32]
+        lib.sref_stepper_cols_nnz.restype = C.c_int64
+        lib.sref_stepper_cols_nnz.argtypes = [_P, C.c_int64, _u32p]
+        lib.sref_stepper_get_cols.argtypes = [_P, C.c_int64, _u32p, _i64p, _u32p, _f64p]
         lib.sref_stepper_init_seeds.argtypes = [_P, _u32p, C.POINTER(CStats)]
         lib.sref_stepper_init_kmeanspp.argtypes = [_P, C.c_uint64, _u32p]
         lib.sref_stepper_step.argtypes = [_P, C.POINTER(CStats)]
@@ -289,12 +294,18 @@ class Stepper:
 
     def __init__(self, corpus: Corpus, k: int, mode="baseline", ncc_epsilon=0.0,
                  conv_sq_dist=1e-4, max_iters=100, threads=0, index_activation_threshold=100,
-                 kind="ref"):
+                 kind="ref", sample=False):
         self.kind = kind
         self.lib = _load(kind)
         self.c = corpus
         self.k = k
-        if kind == "ref":
+        if sample and kind != "ref":
+            raise ValueError("sample steppers (k > n) exist for the compiled reference only")
+        if sample:  # assign-only stepper over a document sample; k may exceed its size
+            h = self.lib.sref_stepper_new_sample(corpus.ref_handle(), k, mode.encode(), ncc_epsilon, threads)
+            if not h:
+                raise ValueError(self.lib.sref_last_error().decode())
+        elif kind == "ref":
             h = self.lib.sref_stepper_new(corpus.ref_handle(), k, mode.encode(), ncc_epsilon,
                                           conv_sq_dist, max_iters, threads,
                                           index_activation_threshold)
@@ -385,6 +396,23 @@ class Stepper:
             self._ck(self.lib.sref_stepper_get_centroids(self.h, ptr, idx, val))
         else:
             self.lib.o_get_centroids(self.h, ptr, idx, val)
+        return ptr, idx[:nnz], val[:nnz]
+
+    def get_cols_csr(self, cols):
+        """CSR (ptr, idx, val) of the centroids `cols` only."""
+        cols = np.ascontiguousarray(cols, np.uint32)
+        if self.kind != "ref":
+            ptr, idx, val = self.get_centroids_csr()
+            parts = [(idx[ptr[j]:ptr[j + 1]], val[ptr[j]:ptr[j + 1]]) for j in cols]
+            p = np.zeros(len(cols) + 1, np.int64)
+            p[1:] = np.cumsum([len(a) for a, _ in parts])
+            return (p, np.concatenate([a for a, _ in parts] + [np.zeros(0, np.uint32)]),
+                    np.concatenate([b for _, b in parts] + [np.zeros(0)]))
+        nnz = self.lib.sref_stepper_cols_nnz(self.h, len(cols), cols)
+        ptr = np.zeros(len(cols) + 1, np.int64)
+        idx = np.zeros(max(nnz, 1), np.uint32)
+        val = np.zeros(max(nnz, 1), np.float64)
+        self._ck(self.lib.sref_stepper_get_cols(self.h, len(cols), cols, ptr, idx, val))
         return ptr, idx[:nnz], val[:nnz]
 
     def get_centroids_dense(self):

@@ -285,6 +285,25 @@ void* sref_stepper_new(void* corpus, std::uint32_t k, const char* mode, double n
     return rc == 0 ? s : nullptr;
 }
 
+// A stepper over a document SAMPLE for teacher-forced assign checks: k may
+// exceed the sample size (config 4: k = 50,000). assign() itself never reads
+// RunConfig::validate's k <= n condition (engine.cpp:218-322).
+void* sref_stepper_new_sample(void* corpus, std::uint32_t k, const char* mode, double ncc_epsilon,
+                              std::uint32_t threads) {
+    Stepper* s = nullptr;
+    int rc = guard([&] {
+        auto* st = new Stepper();
+        st->data = static_cast<CorpusMatrix*>(corpus);
+        st->config.k = k;
+        st->config.mode = parse_mode(mode);
+        st->config.ncc_epsilon = ncc_epsilon;
+        st->config.threads = threads;
+        st->state.unchanged.assign(k, 0);
+        s = st;
+    });
+    return rc == 0 ? s : nullptr;
+}
+
 void sref_stepper_free(void* s) { delete static_cast<Stepper*>(s); }
 
 // BASELINE init: centroid j = document seeds[j], then the nearest-seed
@@ -411,6 +430,31 @@ std::int64_t sref_stepper_centroids_nnz(void* h) {
 
 int sref_stepper_get_centroids(void* h, std::int64_t* ptr, std::uint32_t* idx, double* val) {
     return guard([&] { csr_export(static_cast<Stepper*>(h)->state.centroids, ptr, idx, val); });
+}
+
+// Selected centroids only (large k: the full export is GBs at config 4).
+std::int64_t sref_stepper_cols_nnz(void* h, std::int64_t n, const std::uint32_t* cols) {
+    const auto& c = static_cast<Stepper*>(h)->state.centroids;
+    std::int64_t t = 0;
+    for (std::int64_t q = 0; q < n; ++q) t += static_cast<std::int64_t>(c.at(cols[q]).nnz());
+    return t;
+}
+
+int sref_stepper_get_cols(void* h, std::int64_t n, const std::uint32_t* cols, std::int64_t* ptr,
+                          std::uint32_t* idx, double* val) {
+    return guard([&] {
+        const auto& c = static_cast<Stepper*>(h)->state.centroids;
+        std::int64_t p = 0;
+        ptr[0] = 0;
+        for (std::int64_t q = 0; q < n; ++q) {
+            for (const Entry& e : c.at(cols[q]).entries()) {
+                idx[p] = e.dim;
+                val[p] = e.weight;
+                ++p;
+            }
+            ptr[q + 1] = p;
+        }
+    });
 }
 
 int sref_stepper_set_centroids(void* h, const std::int64_t* ptr, const std::uint32_t* idx,

@@ -98,6 +98,8 @@ SIGNATURES = [
     ("sskm_get_state", C.c_int, [_P, _u32p, _f64p, _u8p]),
     ("sskm_set_state", C.c_int, [_P, _u32p, _f64p, C.c_uint32]),
     ("sskm_get_centroids", C.c_int, [_P, _f32p]),
+    ("sskm_get_centroid_rows", C.c_int, [_P, C.c_uint32, _u32p, _f32p]),
+    ("sskm_get_centroid_cols", C.c_int, [_P, C.c_uint32, _u32p, _f32p]),
     ("sskm_set_centroids", C.c_int, [_P, _f32p]),
     ("sskm_get_repaired", C.c_int, [_P, _u32p, C.POINTER(C.c_uint32)]),
     ("sskm_get_iteration", C.c_int, [_P, C.POINTER(C.c_uint32)]),
@@ -120,14 +122,6 @@ SIGNATURES = [
     ("sskm_postings_work", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     # extension (not in the reference): teacher-forcing of the NCC flags
     ("sskm_set_unchanged", C.c_int, [_P, _u8p]),
-    # synthetic corpus generator (csrc/synth.cpp)
-    ("sskm_synth_last_error", C.c_char_p, []),
-    ("sskm_synth_generate", _P, [C.c_int64, C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
-                                 C.c_uint64, C.c_int]),
-    ("sskm_synth_sizes", None, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_uint32),
-                                C.POINTER(C.c_int64)]),
-    ("sskm_synth_export", None, [_P, _i64p, _i32p, _f32p]),
-    ("sskm_synth_free", None, [_P]),
 ]
 
 _lib = None

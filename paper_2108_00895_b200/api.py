@@ -279,6 +279,22 @@ class Engine:
         check(self.lib.sskm_get_centroids(self.h, out))
         return out
 
+    def get_centroid_rows(self, rows) -> np.ndarray:
+        """Rows of Cᵀ (terms) as a len(rows) × k array."""
+        rows = np.ascontiguousarray(rows, np.uint32)
+        out = np.zeros((len(rows), self.k), np.float32)
+        if len(rows):
+            check(self.lib.sskm_get_centroid_rows(self.h, len(rows), rows, out))
+        return out
+
+    def get_centroid_cols(self, cols) -> np.ndarray:
+        """Columns of Cᵀ (clusters) as a d × len(cols) array."""
+        cols = np.ascontiguousarray(cols, np.uint32)
+        out = np.zeros((self.dims, len(cols)), np.float32)
+        if len(cols):
+            check(self.lib.sskm_get_centroid_cols(self.h, len(cols), cols, out))
+        return out
+
     def set_centroids(self, ct: np.ndarray):
         ct = np.ascontiguousarray(ct, np.float32)
         if ct.shape != (self.dims, self.k):
@@ -329,7 +345,7 @@ def cluster(data: CorpusMatrix, k: int, mode: str = "baseline", seed: int = 0,
             lambdas: Sequence[float] = (0.1, 0.25, 0.4, 0.6), conv_sq_dist: float = 0.0001,
             ncc_epsilon: float = 0.0, index_activation_threshold: int = 100, max_iters: int = 100,
             threads: int = 0, init_seeds=None, device: int = 0,
-            return_centroids: bool = True) -> ClusteringResult:
+            return_centroids: bool = False) -> ClusteringResult:
     """sskm.cluster (bindings.cpp:113-135) on the GPU: the one-shot C-ABI entry
     sskm_cluster_csr = sskm::run (engine.hpp:148). With init_seeds=None the seeds
     come from k-means++ (engine.cpp:66-130) exactly like the reference."""

@@ -900,8 +900,9 @@ __global__ void __launch_bounds__(256) resolve_kernel(ResolveArgs p) {
 }
 
 // ||x_i||² per document (fp64), once per upload.
+// Squared row norms (fp64); flags rows above unit length (bit 32 of *bad).
 __global__ void doc_norm2_kernel(const int64_t* __restrict__ indptr, const float* __restrict__ val, int64_t n,
-                                 double* __restrict__ out) {
+                                 double* __restrict__ out, unsigned int* bad) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
@@ -913,7 +914,10 @@ __global__ void doc_norm2_kernel(const int64_t* __restrict__ indptr, const float
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, off);
-        if (lane == 0) out[i] = q;
+        if (lane == 0) {
+            out[i] = q;
+            if (!(q <= 1.0 + 1e-5)) atomicOr(bad, 32u);
+        }
     }
 }
 

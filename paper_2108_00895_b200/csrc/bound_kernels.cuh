@@ -512,24 +512,46 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
 // hptr[t] = (first pair, count, largest |value| below thr, 0). Pairs beyond
 // `cap` are not written (the host grows the buffer and rebuilds when
 // *total > cap).
+// With the nonzero bitmap nz of Cᵀ (M = Cᵀ; nullptr for other matrices), a
+// 16-byte group of a row is loaded only when one of its 4 columns is marked:
+// unmarked entries are zero, and most of a rare term's row is.
 __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
                                                            uint32_t c0, uint32_t kt, float thr,
                                                            uint4* __restrict__ hptr, uint2* __restrict__ pairs,
                                                            unsigned long long cap, unsigned long long* total,
-                                                           unsigned long long* overflow) {
+                                                           unsigned long long* overflow,
+                                                           const unsigned int* __restrict__ nz) {
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x / kWarp;
     const unsigned lt = (1u << lane) - 1u;
+    const uint32_t kt4 = kt & ~3u;
     for (uint64_t tb = static_cast<uint64_t>(blockIdx.x) * 8; tb < d; tb += static_cast<uint64_t>(gridDim.x) * 8) {
         const uint64_t t = tb + warp;
         const float* row = M + t * ld + c0;
         uint32_t cnt = 0;
         float lowmax = 0.f, allmax = 0.f;
+        // the row's bitmap words of this tile: lane l holds words l and l + 32
+        unsigned ws0 = 0xFFFFFFFFu, ws1 = 0xFFFFFFFFu;
+        if (nz && t < d) {
+            const unsigned int* wrow = nz + t * (ld >> 5) + (c0 >> 5);
+            const uint32_t nw = (kt + 31) / 32;
+            ws0 = static_cast<uint32_t>(lane) < nw ? wrow[lane] : 0u;
+            ws1 = static_cast<uint32_t>(lane) + 32 < nw ? wrow[lane + 32] : 0u;
+        }
+        // marks of this lane's 4 columns 4·lane + 128·it .. + 3 (warp-uniform call)
+        auto bits4 = [&](uint32_t it) -> unsigned {
+            const uint32_t wsel = (static_cast<uint32_t>(lane) >> 3) + 4 * it;  // < 32 for every lane or none
+            const unsigned w = wsel < 32 ? __shfl_sync(0xFFFFFFFFu, ws0, wsel & 31)
+                                         : __shfl_sync(0xFFFFFFFFu, ws1, wsel & 31);
+            return (w >> (4 * (lane & 7))) & 0xFu;
+        };
         if (t < d) {
             // 16-byte loads over the row (tiles start at multiples of 4 columns)
-            const uint32_t kt4 = kt & ~3u;
-            for (uint32_t j = 4u * lane; j < kt4; j += 4u * kWarp) {
+            for (uint32_t it = 0; it * 4u * kWarp < kt4; ++it) {
+                const uint32_t j = 4u * lane + it * 4u * kWarp;
+                const unsigned b4 = bits4(it);
+                if (j >= kt4 || b4 == 0) continue;
                 const float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
                 const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -578,11 +600,11 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
                 // 16-byte loads again (the row is in L1/L2 now); each lane's kept
                 // values go to its prefix position within the 128 columns
                 uint32_t run = 0;
-                const uint32_t kt4 = kt & ~3u;
-                for (uint32_t j0 = 0; j0 < kt4 && run < cnt; j0 += 4u * kWarp) {
-                    const uint32_t j = j0 + 4u * lane;
+                for (uint32_t it = 0; it * 4u * kWarp < kt4 && run < cnt; ++it) {
+                    const uint32_t j = 4u * lane + it * 4u * kWarp;
+                    const unsigned b4 = bits4(it);
                     float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (j < kt4) v4 = __ldg(reinterpret_cast<const float4*>(row + j));
+                    if (j < kt4 && b4 != 0) v4 = __ldg(reinterpret_cast<const float4*>(row + j));
                     const float e[4] = {v4.x, v4.y, v4.z, v4.w};
                     uint32_t mine = 0;
 #pragma unroll

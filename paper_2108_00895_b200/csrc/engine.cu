@@ -195,6 +195,12 @@ public:
     void upload(int64_t n, uint32_t dims, const int64_t* indptr, const int32_t* indices,
                 const float* values, int64_t doc_offset, int64_t n_total) {
         CK(cudaSetDevice(device_));
+        // nothing of the previous corpus / configuration stays usable: the
+        // buffers below are resized for the new corpus, and a failed validation
+        // must not leave a context whose sizes disagree with its buffers
+        corpus_ = false;
+        state_ = false;
+        k_ = 0;
         if (n <= 0) throw InvalidArgument("empty corpus");
         if (dims == 0) throw InvalidArgument("dims must be positive");
         if (indptr[0] != 0) throw InvalidArgument("indptr[0] must be 0");
@@ -235,7 +241,14 @@ public:
             throw InvalidArgument("document weights must be finite with |x| <= 1 (unit-length rows)");
         nonneg_ = (hs_->bad & 16u) == 0;
         xnorm2_.alloc(n);
-        launch(doc_norm2_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p);
+        launch(doc_norm2_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p, &scal_.p->bad);
+        CK_LAUNCH();
+        pull_scalars();
+        // every fixed-point bound (screen accumulators, the int64 sums and their
+        // 128-bit norms) assumes ||x||_2 <= 1: rows must be unit length (fp32
+        // rounding allowed) or shorter, e.g. empty (corpus.cpp:256-261 rejects
+        // any non-unit row of a matrix file)
+        if (hs_->bad & 32u) throw InvalidArgument("row is not unit length (norm above 1)");
         xb_.alloc(n);
         launch(doc_bound_norms_kernel, grid_for(n * 32, 256), 256, indptr_.p, val_.p, n, xnorm2_.p, xb_.p);
         CK_LAUNCH();
@@ -299,13 +312,9 @@ public:
         repaired_flag_.alloc(k_);
         same_.alloc(k_);
         counts_.alloc(k_);
-        rec_ids_.alloc(k_);
-        rec_pos_.alloc(k_);
         chg_ids_.alloc(k_);
         drift_.alloc(k_);
-        norm2_.alloc(k_);
         Q_.alloc(2 * static_cast<size_t>(k_));
-        drift_rec_.alloc(k_);
         part_.alloc(ceil_div(d_, kRowBlock) * k_);
         state_ = false;
         have_cc_ = false;
@@ -710,7 +719,7 @@ public:
         cache_trusted_ = true;
         st->n_unchanged_centroids = iteration_ <= 1 ? 0 : n_unchanged_;
         st->dot_products = static_cast<uint64_t>(k_) * static_cast<uint64_t>(n_);
-        st->gpu_dot_products = st->dot_products + n_exact * k_;
+        st->gpu_dot_products = dots_;
         st->n_changed = k_;
         st->n_rescan = 0;
         st->n_exact = n_exact;
@@ -784,8 +793,7 @@ public:
         const uint64_t n_unch = k_ - n_chg_;
         st->n_unchanged_centroids = static_cast<uint32_t>(n_unch);
         st->dot_products = static_cast<uint64_t>(n_) * n_chg_ + n_rescan * n_unch;
-        st->gpu_dot_products = full_equiv ? static_cast<uint64_t>(n_) * k_
-                                          : static_cast<uint64_t>(n_) * n_chg_ + n_rescan * k_;
+        st->gpu_dot_products = dots_;
         st->n_changed = n_chg_;
         st->n_rescan = n_rescan;
         st->n_exact = n_exact;
@@ -824,6 +832,45 @@ public:
         need_state();
         CK(cudaMemcpy2DAsync(ct, k_ * sizeof(float), ct_.p, ld_ * sizeof(float), k_ * sizeof(float), d_,
                              cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    // Row / column slices of Cᵀ, gathered on the device in bounded chunks.
+    void get_centroid_rows(uint32_t n_rows, const uint32_t* rows, float* out) {
+        need_state();
+        for (uint32_t r = 0; r < n_rows; ++r)
+            if (rows[r] >= d_) throw InvalidArgument("row out of range");
+        const uint32_t per = static_cast<uint32_t>(std::max<uint64_t>(1, (uint64_t(64) << 20) / k_));
+        DevBuf<uint32_t> dids;
+        DevBuf<float> tmp;
+        dids.alloc(per);
+        tmp.alloc(static_cast<size_t>(per) * k_);
+        for (uint32_t r0 = 0; r0 < n_rows; r0 += per) {
+            const uint32_t n = std::min(per, n_rows - r0);
+            CK(cudaMemcpyAsync(dids.p, rows + r0, n * 4, cudaMemcpyHostToDevice, stream_));
+            launch(gather_rows_kernel, grid_for(static_cast<int64_t>(n) * k_, 256), 256, ct_.p, (uint64_t)ld_, k_,
+                   dids.p, n, tmp.p);
+            CK_LAUNCH();
+            CK(cudaMemcpyAsync(out + static_cast<size_t>(r0) * k_, tmp.p, static_cast<size_t>(n) * k_ * 4,
+                               cudaMemcpyDeviceToHost, stream_));
+            CK(cudaStreamSynchronize(stream_));
+        }
+    }
+
+    void get_centroid_cols(uint32_t n_cols, const uint32_t* cols, float* out) {
+        need_state();
+        for (uint32_t c = 0; c < n_cols; ++c)
+            if (cols[c] >= k_) throw InvalidArgument("column out of range");
+        if (n_cols == 0) return;
+        DevBuf<uint32_t> dids;
+        DevBuf<float> tmp;
+        dids.alloc(n_cols);
+        tmp.alloc(static_cast<size_t>(d_) * n_cols);
+        CK(cudaMemcpyAsync(dids.p, cols, n_cols * 4, cudaMemcpyHostToDevice, stream_));
+        launch(gather_cols_kernel, grid_for(static_cast<int64_t>(d_) * n_cols, 256), 256, ct_.p, (uint64_t)ld_, d_,
+               dids.p, n_cols, tmp.p, (uint64_t)n_cols);
+        CK_LAUNCH();
+        CK(cudaMemcpyAsync(out, tmp.p, static_cast<size_t>(d_) * n_cols * 4, cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
     }
 
@@ -1172,26 +1219,17 @@ private:
 
     // Renormalise touched columns, drift, unchanged flags, changed list.
     void finish_update(sskm_iteration_stats* st) {
-        // touched clusters, ascending; their count stays on the device (the
-        // column kernels are sized for k and read it there)
-        launch(compact_ids_kernel, 1, 1024, touched_.p, k_, 1, rec_ids_.p, &scal_.p->n_rec);
-        CK_LAUNCH();
+        // touched columns rewritten group by group (bitmap-driven), drift
+        // partials reduced in a fixed order, then the NCC flags
         const uint32_t n_rb = static_cast<uint32_t>(ceil_div(d_, kRowBlock));
-        const unsigned* n_rec_dev = &scal_.p->n_rec;
-        {
-            dim3 grid(static_cast<unsigned>(ceil_div(k_, 128)), n_rb);
-            launch(q_norm2_kernel, static_cast<unsigned>(ceil_div(k_, 128)), 128, Q_.p, rec_ids_.p, n_rec_dev,
-                   norm2_.p);
-            launch(write_cols_kernel, grid, 128, S_.p, ct_.p, ld_, d_, rec_ids_.p, n_rec_dev, k_, norm2_.p, part_.p,
-                   &scal_.p->zero_flag, nz_.p);
-            launch(reduce_partials_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 256, part_.p, n_rb, n_rec_dev, k_,
-                   drift_rec_.p);
-            launch(scatter_pos_dev_kernel, grid_for(k_, 256), 256, rec_ids_.p, n_rec_dev, rec_pos_.p);
-            CK_LAUNCH();
-        }
-        launch(flags_kernel, grid_for(k_, 256), 256, 
-            k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon, touched_.p, repaired_flag_.p, rec_pos_.p,
-            drift_rec_.p, unchanged_.p, same_.p, drift_.p, &scal_.p->max_drift_bits, &scal_.p->n_unchanged);
+        const uint32_t n_groups = static_cast<uint32_t>(ceil_div(k_, 32));
+        launch(write_groups_kernel, dim3(static_cast<unsigned>(ceil_div(n_groups, 4)), n_rb), 128, S_.p, ct_.p,
+               (uint64_t)ld_, d_, k_, touched_.p, Q_.p, part_.p, &scal_.p->zero_flag, nz_.p);
+        launch(reduce_groups_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 256, part_.p, n_rb, k_, touched_.p,
+               drift_.p, &scal_.p->n_rec);
+        launch(flags_kernel, grid_for(k_, 256), 256, k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon,
+               repaired_flag_.p, drift_.p, unchanged_.p, same_.p, &scal_.p->max_drift_bits,
+               &scal_.p->n_unchanged);
         CK_LAUNCH();
         CK(cudaMemsetAsync(touched_.p, 0, k_, stream_));
         ++updates_since_assign_;
@@ -1235,6 +1273,7 @@ private:
         screen_launches_ = 0;
         bstat_docs_ = bstat_pairs_ = bstat_cand_ = bstat_doc_nnz_ = bstat_cand_nnz_ = bstat_visits_ = bstat_own_ = 0;
         bstat_theta_ = 0.0;
+        dots_ = 0;
         CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
         CK(cudaMemcpyAsync(sims_start_.p, sims_.p, n_ * 8, cudaMemcpyDeviceToDevice, stream_));
     }
@@ -1296,6 +1335,7 @@ private:
         p.n_rescan = &scal_.p->n_rescan;
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
             1, std::min<int64_t>(static_cast<int64_t>(sms_) * blocks_per_sm_, ceil_div(n_work, 8))));
+        dots_ += static_cast<uint64_t>(n_work) * ncols;  // every (document, column) pair, exact fp64
         for (uint32_t c0 = 0; c0 < ncols; c0 += W) {
             p.col0 = c0;
             p.first = c0 == 0;
@@ -1407,6 +1447,7 @@ private:
         const uint64_t n_list = n_work > 0 ? static_cast<uint64_t>(n_work) - std::min<uint64_t>(n_fb, n_work) : 0;
         bstat_docs_ += n_list;
         bstat_pairs_ += ctr[1];
+        dots_ += ctr[0] + ctr[3];  // exact fp64 dots: candidates and own-cluster dots
         bstat_cand_ += ctr[0];
         bstat_visits_ += ctr[2];
         bstat_own_ += ctr[3];
@@ -1506,8 +1547,11 @@ private:
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 32));
         for (int attempt = 0; attempt < 2; ++attempt) {
             CK(cudaMemsetAsync(hpctr_.p, 0, 2 * sizeof(unsigned long long), stream_));
+            // the screen addresses pairs with 32-bit offsets: lists past 2^32 are
+            // dropped (exact, looser bound) rather than truncated
             launch(hipost_build_kernel, grid, 256, M, ld, d_, c0, kt, thr, hptr_.p, pairs_.p,
-                   static_cast<unsigned long long>(pairs_.n), hpctr_.p, hpctr_.p + 1);
+                   std::min<unsigned long long>(pairs_.n, 0xFFFFFFFFull), hpctr_.p, hpctr_.p + 1,
+                   M == ct_.p ? static_cast<const unsigned int*>(nz_.p) : nullptr);
             CK_LAUNCH();
             if (!check) return;
             unsigned long long total = 0;
@@ -1584,6 +1628,7 @@ private:
 
     void postings_screen(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
                          const uint32_t* order, int64_t n_work, int fuse) {
+        dots_ += static_cast<uint64_t>(n_work) * (ncols + 1);  // fp32 screen dots + the certified exact one
         sb_.alloc(n_);
         ss_.alloc(n_);
         sa_.alloc(n_);
@@ -1697,6 +1742,7 @@ private:
 
     void screen_tiles(const float* M, uint64_t ld, uint32_t ncols, const uint32_t* col_ids, const uint32_t* skip,
                       const uint32_t* order, int64_t n_work) {
+        dots_ += static_cast<uint64_t>(n_work) * (ncols + 1);  // fp32 screen dots + the certified exact one
         sb_.alloc(n_);
         ss_.alloc(n_);
         sa_.alloc(n_);
@@ -1836,7 +1882,7 @@ private:
     int sms_ = 148;
     cudaStream_t stream_{};
     cudaEvent_t ev_[10]{};
-    static constexpr int kUserEvents = 16;
+    static constexpr int kUserEvents = 256;
     cudaEvent_t user_ev_[kUserEvents]{};
     uint64_t launches_ = 0;
     uint64_t tile_bytes_ = 64ull << 20;
@@ -1880,7 +1926,7 @@ private:
     uint64_t last_n_rescan_ = 0;
     DevBuf<float> ct_, cc_;
     DevBuf<long long> S_;
-    DevBuf<uint32_t> a_, a_sum_, a_start_, moved_, rescan_, rec_ids_, rec_pos_, chg_ids_;
+    DevBuf<uint32_t> a_, a_sum_, a_start_, moved_, rescan_, chg_ids_;
     DevBuf<double> sims_start_, xnorm2_;
     DevBuf<float> sb_, ss_;
     DevBuf<uint32_t> pcnt_, pptr_;
@@ -1916,6 +1962,7 @@ private:
              bstat_visits_ = 0, bstat_own_ = 0;
     uint32_t updates_since_assign_ = 0;  // updates since the last assign (the same_ flags' validity)
     double bstat_theta_ = 0.0;
+    uint64_t dots_ = 0;  // dots the kernels evaluated in the current assign (gpu_dot_products)
     bool nonneg_ = true;
     double last_density_ = 0.0;
     double dense_above_ = 0.15;
@@ -1923,7 +1970,7 @@ private:
     double ncc_full_frac_ = 0.25;
     DevBuf<uint32_t> sa_, exact_;
     DevBuf<uint32_t> order_, keys32_;
-    DevBuf<double> sims_, drift_, norm2_, drift_rec_, part_, obj_part_;
+    DevBuf<double> sims_, drift_, part_, obj_part_;
     DevBuf<unsigned long long> Q_;  // exact Σ_t S[t][j]² per column (128-bit: lo, hi)
     DevBuf<unsigned int> nz_;       // a bit per (term, cluster): S or Cᵀ may be nonzero there
     DevBuf<uint8_t> unchanged_, touched_, repaired_flag_;
@@ -2110,6 +2157,14 @@ int sskm_set_unchanged(sskm_ctx* ctx, const uint8_t* flags) {
 
 int sskm_get_centroids(sskm_ctx* ctx, float* ct) {
     return guard([&] { E(ctx).get_centroids(ct); });
+}
+
+int sskm_get_centroid_rows(sskm_ctx* ctx, uint32_t n_rows, const uint32_t* rows, float* out) {
+    return guard([&] { E(ctx).get_centroid_rows(n_rows, rows, out); });
+}
+
+int sskm_get_centroid_cols(sskm_ctx* ctx, uint32_t n_cols, const uint32_t* cols, float* out) {
+    return guard([&] { E(ctx).get_centroid_cols(n_cols, cols, out); });
 }
 
 int sskm_set_centroids(sskm_ctx* ctx, const float* ct) {

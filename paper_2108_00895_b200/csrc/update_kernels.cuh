@@ -187,18 +187,6 @@ __global__ void delta_packed_kernel(int64_t n_moved, const uint32_t* __restrict_
     }
 }
 
-// ‖S_j‖² of the recomputed columns from the exact 128-bit Q_j (< 2^124, ≥ 0).
-// The column count n is read on the device (no host round trip).
-__global__ void q_norm2_kernel(const unsigned long long* __restrict__ Q, const uint32_t* __restrict__ ids,
-                               const unsigned int* __restrict__ n_dev, double* __restrict__ norm2) {
-    const uint32_t n_ids = *n_dev;
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_ids; c += gridDim.x * blockDim.x) {
-        const uint32_t j = ids[c];
-        const unsigned long long lo = Q[2ull * j], hi = Q[2ull * j + 1];
-        norm2[c] = static_cast<double>(hi) * 0x1p64 + static_cast<double>(lo);
-    }
-}
-
 // Multi-GPU delta exchange: per moved document its (old, new) clusters and
 // row length, then (after a scan) the rows themselves, packed contiguously.
 __global__ void moved_meta_kernel(const uint32_t* __restrict__ moved, const unsigned long long* n_moved_p,
@@ -279,82 +267,108 @@ __global__ void compact_ids_kernel(const uint8_t* __restrict__ flags, uint32_t k
 
 constexpr int kRowBlock = 512;  // rows per partial in the column reductions
 
-// Column sums of the row-block partials part[rb][c] (row stride `stride`), in
-// a fixed association: 8 segments of row blocks summed in order by 8 threads
-// of a column, then the 8 segment sums in order. Deterministic; 32 columns per
-// 256-thread block.
-__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ part, uint32_t n_rb,
-                                                              const unsigned int* __restrict__ n_dev,
-                                                              uint32_t stride, double* __restrict__ out) {
+// Rewrite of the touched columns: c = S · (1/‖S‖) in fp64, stored fp32, with
+// the squared drift against the previous fp32 column as fixed-order partials.
+// (The reference divides by the norm and iterates to a fixpoint,
+// sparse_vector.cpp:160-209; both land within one fp64 ulp, below fp32
+// resolution.) The norm comes straight from the exact 128-bit Q_j.
+//
+// Work by 32-column groups (the bitmap's words): a warp owns group g (lane =
+// column 32g + lane) over one block of kRowBlock rows. Rows are visited 32 at a
+// time through their bitmap words (lane r loads row r's word), and only rows
+// where some touched column of the group is marked are read: an unmarked
+// (t, j) has S = 0 and Cᵀ = 0, and on the TF-IDF corpora most (row, group)
+// words are empty, so most of S and Cᵀ is never read. Per (row block, column)
+// the drift partial is an ascending-row fp64 sum (unmarked rows would add
+// exact zeros); the partials are reduced in a fixed association below.
+__global__ void __launch_bounds__(128) write_groups_kernel(const long long* __restrict__ S, float* __restrict__ CT,
+                                                           uint64_t ld, uint32_t d, uint32_t k,
+                                                           const uint8_t* __restrict__ touched,
+                                                           const unsigned long long* __restrict__ Q,
+                                                           double* __restrict__ part, unsigned int* zero_flag,
+                                                           unsigned int* __restrict__ nz) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const uint32_t g = blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+    const uint32_t rb = blockIdx.y;
+    const uint32_t j = g * kWarp + lane;
+    if (g * kWarp >= k) return;
+    const bool active = j < k && touched[j] != 0;
+    const unsigned amask = __ballot_sync(0xFFFFFFFFu, active);
+    if (amask == 0) return;
+    double inv = 0.0;
+    if (active) {
+        const double n2 = static_cast<double>(Q[2ull * j + 1]) * 0x1p64 + static_cast<double>(Q[2ull * j]);
+        const double nrm = sqrt(n2);
+        if (nrm == 0.0 && rb == 0) atomicOr(zero_flag, 1u);  // normalize() of the zero vector throws
+        inv = nrm == 0.0 ? 0.0 : 1.0 / nrm;
+    }
+    const unsigned lbit = 1u << lane;
+    const uint64_t wpr = ld >> 5;
+    const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
+    double dr = 0.0;
+    for (uint32_t tb = t0; tb < t1; tb += kWarp) {
+        const uint32_t tr = tb + lane;
+        const unsigned wr = tr < t1 ? nz[static_cast<uint64_t>(tr) * wpr + g] & amask : 0u;
+        unsigned rows = __ballot_sync(0xFFFFFFFFu, wr != 0);
+        // four marked rows per round: all loads of a round before its stores
+        while (rows) {
+            int r[4];
+            unsigned w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                r[q] = rows ? __ffs(rows) - 1 : -1;
+                if (rows) rows &= rows - 1;
+                w[q] = __shfl_sync(0xFFFFFFFFu, wr, r[q] < 0 ? 0 : r[q]);
+            }
+            long long sv[4];
+            float old[4];
+            bool on[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                on[q] = r[q] >= 0 && (w[q] & lbit);
+                const uint64_t o = static_cast<uint64_t>(tb + r[q]) * ld + j;
+                sv[q] = on[q] ? __ldcs(S + o) : 0;
+                old[q] = on[q] ? CT[o] : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!on[q]) continue;
+                const uint64_t o = static_cast<uint64_t>(tb + r[q]) * ld + j;
+                const float cn = sv[q] == 0 ? 0.f : static_cast<float>(static_cast<double>(sv[q]) * inv);
+                const double diff = static_cast<double>(cn) - static_cast<double>(old[q]);
+                dr = fma(diff, diff, dr);
+                if (cn != old[q]) CT[o] = cn;
+                if (sv[q] == 0) atomicAnd(nz + static_cast<uint64_t>(tb + r[q]) * wpr + g, ~lbit);
+            }
+        }
+    }
+    if (active) part[static_cast<uint64_t>(rb) * k + j] = dr;
+}
+
+// Per touched column: the row-block partials of write_groups_kernel summed in a
+// fixed association (8 segments of row blocks in order, then the 8 segment sums
+// in order: deterministic); the count of touched columns.
+__global__ void __launch_bounds__(256) reduce_groups_kernel(const double* __restrict__ part, uint32_t n_rb, uint32_t k,
+                                                            const uint8_t* __restrict__ touched,
+                                                            double* __restrict__ drift, unsigned int* n_rec) {
     __shared__ double sh[8][32];
-    const uint32_t n_ids = *n_dev;
     const uint32_t cl = threadIdx.x & 31, seg = threadIdx.x >> 5;
     const uint32_t c = blockIdx.x * 32 + cl;
+    const bool on = c < k && touched[c] != 0;
     const uint32_t per = (n_rb + 7) / 8;
     double s = 0.0;
-    if (c < n_ids)
-        for (uint32_t rb = seg * per; rb < min(n_rb, (seg + 1) * per); ++rb)
-            s += part[static_cast<uint64_t>(rb) * stride + c];
+    if (on)
+        for (uint32_t rb = seg * per; rb < min(n_rb, (seg + 1) * per); ++rb) s += part[static_cast<uint64_t>(rb) * k + c];
     sh[seg][cl] = s;
     __syncthreads();
-    if (seg == 0 && c < n_ids) {
+    if (seg == 0 && c < k) {
         double t = 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) t += sh[q][cl];
-        out[c] = t;
+        drift[c] = on ? t : 0.0;
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, on);
+        if (cl == 0 && b) atomicAdd(n_rec, static_cast<unsigned>(__popc(b)));
     }
-}
-
-// Rewrite recomputed columns: c = S · (1/||S||) in fp64, stored fp32, with the
-// squared drift against the previous fp32 column as fixed-order partials. (The
-// reference divides by the norm and iterates to a fixpoint, sparse_vector.cpp:
-// 160-209; both land within one fp64 ulp, below fp32 resolution.)
-__global__ void write_cols_kernel(const long long* __restrict__ S, float* __restrict__ CT,
-                                  uint64_t ld, uint32_t d, const uint32_t* __restrict__ ids,
-                                  const unsigned int* __restrict__ n_dev, uint32_t stride,
-                                  const double* __restrict__ norm2, double* __restrict__ part,
-                                  unsigned int* zero_flag, unsigned int* __restrict__ nz) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t rb = blockIdx.y;
-    if (c >= *n_dev) return;
-    const uint32_t j = ids[c];
-    const double nrm = sqrt(norm2[c]);
-    if (nrm == 0.0) {  // normalize() of the zero vector throws (sparse_vector.cpp:161)
-        if (rb == 0) atomicOr(zero_flag, 1u);
-        return;
-    }
-    const double inv = 1.0 / nrm;
-    const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
-    // unmarked (t, j) have S = 0 and Cᵀ = 0: nothing to read or write (the marks
-    // are a superset: set by the delta kernels, cleared here once an entry is 0)
-    const uint64_t wpr = ld >> 5;
-    const uint32_t gw = j >> 5, gb = 1u << (j & 31u);
-    double dr = 0.0;
-    // 8 rows per step, all loads issued before any store (the compiler cannot
-    // prove the Cᵀ store of one row does not alias the next row's load)
-    constexpr int kB = 8;
-    for (uint32_t tb = t0; tb < t1; tb += kB) {
-        long long q[kB];
-        float old[kB];
-        bool on[kB];
-#pragma unroll
-        for (int r = 0; r < kB; ++r) on[r] = tb + r < t1 && (nz[static_cast<uint64_t>(tb + r) * wpr + gw] & gb);
-#pragma unroll
-        for (int r = 0; r < kB; ++r) {
-            const uint64_t o = static_cast<uint64_t>(tb + r) * ld + j;
-            q[r] = on[r] ? __ldcs(S + o) : 0;
-            old[r] = on[r] ? CT[o] : 0.f;
-        }
-#pragma unroll
-        for (int r = 0; r < kB; ++r) {
-            const float cn = q[r] == 0 ? 0.f : static_cast<float>(static_cast<double>(q[r]) * inv);
-            const double diff = static_cast<double>(cn) - static_cast<double>(old[r]);
-            dr = fma(diff, diff, dr);
-            if (cn != old[r]) CT[static_cast<uint64_t>(tb + r) * ld + j] = cn;
-            if (on[r] && q[r] == 0) atomicAnd(nz + static_cast<uint64_t>(tb + r) * wpr + gw, ~gb);
-        }
-    }
-    part[static_cast<uint64_t>(rb) * stride + c] = dr;
 }
 
 // Repair candidates: (orderable(sim), doc) keys for one stable radix sort.
@@ -383,15 +397,12 @@ __global__ void apply_moves_kernel(const uint32_t* __restrict__ pairs, uint32_t 
 // same[j]: column j is bit-identical to its value before this update (not
 // rewritten, or rewritten with zero drift: Σ(new − old)² = 0 in fp64 of fp32
 // differences only for equal columns) — the bound screen's cached-similarity test.
-__global__ void flags_kernel(uint32_t k, int first_iter, double eps, const uint8_t* __restrict__ touched,
-                             const uint8_t* __restrict__ repaired, const uint32_t* __restrict__ rec_pos,
-                             const double* __restrict__ drift_rec, uint8_t* __restrict__ unchanged,
-                             uint8_t* __restrict__ same, double* __restrict__ drift_out,
-                             unsigned long long* max_drift_bits, unsigned int* n_unchanged) {
+__global__ void flags_kernel(uint32_t k, int first_iter, double eps, const uint8_t* __restrict__ repaired,
+                             const double* __restrict__ drift, uint8_t* __restrict__ unchanged,
+                             uint8_t* __restrict__ same, unsigned long long* max_drift_bits,
+                             unsigned int* n_unchanged) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
-        double dj = 0.0;
-        if (touched[j]) dj = drift_rec[rec_pos[j]];
-        drift_out[j] = dj;
+        const double dj = drift[j];  // 0 for untouched columns
         same[j] = (!first_iter && !repaired[j] && dj == 0.0) ? 1 : 0;
         uint8_t u;
         if (first_iter) {
@@ -411,13 +422,6 @@ __global__ void scatter_pos_kernel(const uint32_t* __restrict__ ids, uint32_t n,
         pos[ids[c]] = c;
 }
 
-__global__ void scatter_pos_dev_kernel(const uint32_t* __restrict__ ids, const unsigned int* __restrict__ n_dev,
-                                       uint32_t* __restrict__ pos) {
-    const uint32_t n = *n_dev;
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
-        pos[ids[c]] = c;
-}
-
 // Compact copy of the changed columns for the NCC scan: CC[t][c] = Cᵀ[t][ids[c]],
 // zero-padded to ld_cc.
 __global__ void gather_cols_kernel(const float* __restrict__ CT, uint64_t ld, uint32_t d,
@@ -429,6 +433,17 @@ __global__ void gather_cols_kernel(const float* __restrict__ CT, uint64_t ld, ui
         const uint64_t t = o / ld_cc;
         const uint32_t c = static_cast<uint32_t>(o - t * ld_cc);
         CC[o] = c < n_ids ? CT[t * ld + ids[c]] : 0.f;
+    }
+}
+
+// Rows rows[0..n) of Cᵀ, densely packed: out[r][j] = Cᵀ[rows[r]][j], j < k.
+__global__ void gather_rows_kernel(const float* __restrict__ CT, uint64_t ld, uint32_t k,
+                                   const uint32_t* __restrict__ rows, uint32_t n, float* __restrict__ out) {
+    const uint64_t total = static_cast<uint64_t>(n) * k;
+    for (uint64_t o = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; o < total;
+         o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = o / k;
+        out[o] = CT[static_cast<uint64_t>(rows[r]) * ld + (o - r * k)];
     }
 }
 
