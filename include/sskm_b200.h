@@ -162,6 +162,34 @@ int sskm_set_unchanged(sskm_ctx* ctx, const uint8_t* unchanged);
 int sskm_get_repaired(sskm_ctx* ctx, uint32_t* repaired, uint32_t* n_repaired);
 int sskm_get_iteration(sskm_ctx* ctx, uint32_t* iteration);
 
+/* Multi-device context (SURVEY §8b sskm_cuda_open(n_dev, devs)): one host
+ * thread drives the listed GPUs; documents are sharded in contiguous equal
+ * ranges, centroids and the exact integer cluster sums replicated. Each
+ * iteration every device applies every shard's moved rows to its own sums,
+ * reading the peers' shards over NVLink (peer access): no gather, no
+ * collective library. Assignments, sims and centroids are bitwise those of a
+ * single device. The calls mirror the single-device ones above. */
+typedef struct sskm_multi sskm_multi;
+int sskm_multi_open(int32_t n_devices, const int32_t* devices, sskm_multi** out);
+int sskm_multi_close(sskm_multi* ctx);
+int sskm_multi_upload_csr(sskm_multi* ctx, int64_t n_docs, uint32_t dims, const int64_t* indptr,
+                          const int32_t* indices, const float* values);
+int sskm_multi_configure(sskm_multi* ctx, const sskm_run_config* cfg);
+int sskm_multi_init_from_seeds(sskm_multi* ctx, const uint32_t* seeds);
+int sskm_multi_step(sskm_multi* ctx, sskm_iteration_stats* st);
+int sskm_multi_run(sskm_multi* ctx, sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters,
+                   int32_t* stop_reason);
+int sskm_multi_get_state(sskm_multi* ctx, uint32_t* assignments, double* sims);
+int sskm_multi_get_centroids(sskm_multi* ctx, float* ct);
+int sskm_multi_launch_count(sskm_multi* ctx, uint64_t* n);
+/* sskm::run (engine.hpp:148) over several devices, as sskm_cluster_csr below;
+ * needs the seeds (k-means++ seeding is single-device). */
+int sskm_cluster_csr_multi(const sskm_run_config* cfg, int32_t n_devices, const int32_t* devices, int64_t n_docs,
+                           uint32_t dims, const int64_t* indptr, const int32_t* indices, const float* values,
+                           const uint32_t* seeds, uint32_t* assignments, double* sims, float* ct,
+                           sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters,
+                           int32_t* stop_reason, double* objective);
+
 /* Device timing on the context's stream (CUDA events; 256 slots) and the
  * number of kernels this context has launched — the bench's live evidence. */
 int sskm_timer_record(sskm_ctx* ctx, int32_t slot);

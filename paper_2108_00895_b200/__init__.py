@@ -11,6 +11,7 @@ from .api import (
     CorpusMatrix,
     Engine,
     IterationStats,
+    MultiEngine,
     SparseVector,
     cluster,
     parse_mode,
@@ -31,6 +32,7 @@ __all__ = [
     "CorpusMatrix",
     "Engine",
     "IterationStats",
+    "MultiEngine",
     "SparseVector",
     "cluster",
     "parse_mode",

@@ -107,6 +107,20 @@ SIGNATURES = [
                                    _ST, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_double)]),
     ("sskm_release_cache", C.c_int, []),
+    # multi-device context (one host thread, several GPUs, peer-memory exchange)
+    ("sskm_multi_open", C.c_int, [C.c_int32, _i32p, C.POINTER(_P)]),
+    ("sskm_multi_close", C.c_int, [_P]),
+    ("sskm_multi_upload_csr", C.c_int, [_P, C.c_int64, C.c_uint32, _i64p, _i32p, _f32p]),
+    ("sskm_multi_configure", C.c_int, [_P, _CFG]),
+    ("sskm_multi_init_from_seeds", C.c_int, [_P, _u32p]),
+    ("sskm_multi_step", C.c_int, [_P, _ST]),
+    ("sskm_multi_run", C.c_int, [_P, _ST, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int32)]),
+    ("sskm_multi_get_state", C.c_int, [_P, _P, _P]),
+    ("sskm_multi_get_centroids", C.c_int, [_P, _f32p]),
+    ("sskm_multi_launch_count", C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    ("sskm_cluster_csr_multi", C.c_int, [_CFG, C.c_int32, _i32p, C.c_int64, C.c_uint32, _i64p, _i32p, _f32p, _P,
+                                         _P, _P, _P, _ST, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_double)]),
     ("sskm_local_counts", C.c_int, [_P, _i64p]),
     ("sskm_local_candidates", C.c_int, [_P, C.c_int64, _f64p, _i64p, _u32p, C.POINTER(C.c_int64)]),
     ("sskm_move_doc", C.c_int, [_P, C.c_int64, C.c_uint32]),

@@ -335,6 +335,74 @@ class Engine:
         return int(it.value)
 
 
+class MultiEngine:
+    """Several GPUs of one node driven from this thread (sskm_multi_*): the
+    corpus is sharded over `devices` in contiguous equal ranges; every device
+    applies every shard's moved rows to its own exact sums through peer memory,
+    so assignments, sims and centroids equal a single-GPU run bit for bit."""
+
+    def __init__(self, devices: Sequence[int]):
+        self.lib = _lib.load()
+        self.devices = [int(d) for d in devices]
+        self.h = C.c_void_p()
+        check(self.lib.sskm_multi_open(len(self.devices), np.asarray(self.devices, np.int32), C.byref(self.h)))
+        self.n = self.k = self.dims = 0
+
+    def close(self):
+        if self.h:
+            check(self.lib.sskm_multi_close(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, data: CorpusMatrix):
+        check(self.lib.sskm_multi_upload_csr(self.h, data.n_docs, data.dims, data.indptr, data.indices, data.values))
+        self.n, self.dims = data.n_docs, data.dims
+
+    def configure(self, k, **kw):
+        self.cfg = make_config(k, **kw)
+        check(self.lib.sskm_multi_configure(self.h, C.byref(self.cfg)))
+        self.k = int(k)
+
+    def init_from_seeds(self, seeds):
+        s = np.ascontiguousarray(seeds, dtype=np.uint32)
+        if len(s) != self.k:
+            raise ValueError("need exactly k seeds")
+        check(self.lib.sskm_multi_init_from_seeds(self.h, s))
+
+    def step(self) -> IterationStats:
+        st = sskm_iteration_stats()
+        check(self.lib.sskm_multi_step(self.h, C.byref(st)))
+        return IterationStats.from_c(st)
+
+    def run(self):
+        cap = int(self.cfg.max_iters)
+        stats = (sskm_iteration_stats * cap)()
+        n_it, stop = C.c_uint32(), C.c_int32()
+        check(self.lib.sskm_multi_run(self.h, stats, cap, C.byref(n_it), C.byref(stop)))
+        return [IterationStats.from_c(stats[i]) for i in range(n_it.value)], STOP_REASONS[stop.value]
+
+    def get_state(self):
+        a = np.zeros(self.n, np.uint32)
+        s = np.zeros(self.n, np.float64)
+        check(self.lib.sskm_multi_get_state(self.h, a.ctypes.data, s.ctypes.data))
+        return a, s
+
+    def get_centroids(self) -> np.ndarray:
+        out = np.zeros((self.dims, self.k), np.float32)
+        check(self.lib.sskm_multi_get_centroids(self.h, out))
+        return out
+
+    def launch_count(self) -> int:
+        n = C.c_uint64()
+        check(self.lib.sskm_multi_launch_count(self.h, C.byref(n)))
+        return int(n.value)
+
+
 def validate(n_docs: int, k: int, **kw) -> None:
     """RunConfig::validate (engine.cpp:47-64)."""
     cfg = make_config(k, **{x: y for x, y in kw.items() if x != "threads"})
@@ -344,11 +412,14 @@ def validate(n_docs: int, k: int, **kw) -> None:
 def cluster(data: CorpusMatrix, k: int, mode: str = "baseline", seed: int = 0,
             lambdas: Sequence[float] = (0.1, 0.25, 0.4, 0.6), conv_sq_dist: float = 0.0001,
             ncc_epsilon: float = 0.0, index_activation_threshold: int = 100, max_iters: int = 100,
-            threads: int = 0, init_seeds=None, device: int = 0,
+            threads: int = 0, init_seeds=None, device: int = 0, devices: Optional[Sequence[int]] = None,
             return_centroids: bool = False) -> ClusteringResult:
     """sskm.cluster (bindings.cpp:113-135) on the GPU: the one-shot C-ABI entry
     sskm_cluster_csr = sskm::run (engine.hpp:148). With init_seeds=None the seeds
-    come from k-means++ (engine.cpp:66-130) exactly like the reference."""
+    come from k-means++ (engine.cpp:66-130) exactly like the reference.
+    devices=[...] shards the documents over several GPUs of this node
+    (sskm_cluster_csr_multi; needs init_seeds); the result is bitwise the
+    single-GPU one."""
     if not isinstance(data, CorpusMatrix):
         raise TypeError("data must be a CorpusMatrix")
     lib = _lib.load()
@@ -371,10 +442,19 @@ def cluster(data: CorpusMatrix, k: int, mode: str = "baseline", seed: int = 0,
         seeds = np.ascontiguousarray(init_seeds, np.uint32)
         if len(seeds) != k:
             raise ValueError("init_seeds must hold exactly k document ids")
-    check(lib.sskm_cluster_csr(C.byref(cfg), n, data.dims, data.indptr, data.indices, data.values,
-                               seeds.ctypes.data if seeds is not None else None, a.ctypes.data,
-                               s.ctypes.data, ct.ctypes.data if ct is not None else None, stats, max_iters,
-                               C.byref(n_it), C.byref(stop), C.byref(obj)))
+    if devices is not None:
+        devs = np.ascontiguousarray([int(x) for x in devices], np.int32)
+        if seeds is None:
+            raise ValueError("a multi-device run needs init_seeds (k-means++ runs on one device)")
+        check(lib.sskm_cluster_csr_multi(C.byref(cfg), len(devs), devs, n, data.dims, data.indptr, data.indices,
+                                         data.values, seeds.ctypes.data, a.ctypes.data, s.ctypes.data,
+                                         ct.ctypes.data if ct is not None else None, stats, max_iters,
+                                         C.byref(n_it), C.byref(stop), C.byref(obj)))
+    else:
+        check(lib.sskm_cluster_csr(C.byref(cfg), n, data.dims, data.indptr, data.indices, data.values,
+                                   seeds.ctypes.data if seeds is not None else None, a.ctypes.data,
+                                   s.ctypes.data, ct.ctypes.data if ct is not None else None, stats, max_iters,
+                                   C.byref(n_it), C.byref(stop), C.byref(obj)))
     its = [IterationStats.from_c(stats[i]) for i in range(n_it.value)]
     return ClusteringResult(assignments=a, sims=s, iterations=its, objective=obj.value,
                             stop_reason=STOP_REASONS[stop.value], centroids=ct, seeds=seeds,

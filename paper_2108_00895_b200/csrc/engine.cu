@@ -453,7 +453,7 @@ public:
         launch(moved_kernel, grid_for(n_, 256), 256, a_.p, a_sum_.p, n_, moved_.p, &scal_.p->n_moved);
         CK_LAUNCH();
         launch(delta_local_kernel, grid_for(n_ * 32, 256), 256, 
-            indptr_.p, idx_.p, val_.p, moved_.p, &scal_.p->n_moved, a_.p, a_sum_.p, S_.p, ld_, K_,
+            indptr_.p, idx_.p, val_.p, moved_.p, &scal_.p->n_moved, a_.p, a_sum_.p, a_sum_.p, S_.p, ld_, K_,
             touched_.p, Q_.p, nz_.p);
         CK_LAUNCH();
         finish_update(st);
@@ -489,6 +489,131 @@ public:
         CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
         st->update_ms = ms;
         st->n_moved = static_cast<uint64_t>(n_moved);
+    }
+
+    // ------------------------------------------------ multi-device phases --
+    // The update of a MultiEngine step (multi.cuh), split at its exchange
+    // points. Every device holds the full sums S and applies the moved rows of
+    // every shard itself, reading the peers' shards over NVLink.
+    struct PeerView {
+        const int64_t* indptr;
+        const int32_t* idx;
+        const float* val;
+        const uint32_t* moved;
+        const unsigned long long* n_moved;
+        const uint32_t* a;
+        const uint32_t* a_sum;
+        int64_t n;
+    };
+    PeerView peer_view() const {
+        return {indptr_.p, idx_.p, val_.p, moved_.p, &scal_.p->n_moved, a_.p, a_sum_.p, n_};
+    }
+    int device() const { return device_; }
+    int64_t doc_offset() const { return doc_offset_; }
+
+    // 1. local cluster sizes, copied to the host
+    void mp_begin(unsigned long long* counts_host) {
+        need_state();
+        CK(cudaSetDevice(device_));
+        CK(cudaEventRecord(ev_[0], stream_));
+        iteration_ += 1;
+        repaired_.clear();
+        local_counts_device();
+        CK(cudaMemcpyAsync(counts_host, counts_.p, k_ * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           stream_));
+        pull_scalars();
+        if (hs_->bad) throw InvalidArgument("assignment out of range");
+    }
+
+    // 2. this step's repairs (moves of local documents, as (local doc, cluster)
+    // pairs; the repaired clusters of every device), then the moved list
+    void mp_moved(const std::vector<uint32_t>& local_moves, const std::vector<uint32_t>& repaired,
+                  cudaEvent_t done) {
+        CK(cudaSetDevice(device_));
+        repaired_ = repaired;
+        CK(cudaMemsetAsync(repaired_flag_.p, 0, k_, stream_));
+        if (!repaired.empty()) {
+            std::vector<uint8_t> f(k_, 0);
+            for (uint32_t j : repaired) f[j] = 1;
+            CK(cudaMemcpyAsync(repaired_flag_.p, f.data(), k_, cudaMemcpyHostToDevice, stream_));
+        }
+        if (!local_moves.empty()) {
+            CK(cudaMemcpyAsync(moves_.p, local_moves.data(), local_moves.size() * 4, cudaMemcpyHostToDevice,
+                               stream_));
+            launch(apply_moves_kernel, 1, 256, moves_.p, static_cast<uint32_t>(local_moves.size() / 2), a_.p);
+        }
+        reset_scalars();
+        launch(moved_kernel, grid_for(n_, 256), 256, a_.p, a_sum_.p, n_, moved_.p, &scal_.p->n_moved);
+        CK_LAUNCH();
+        CK(cudaEventRecord(done, stream_));
+        if (!repaired.empty() || !local_moves.empty()) CK(cudaStreamSynchronize(stream_));  // host vectors
+    }
+
+    // 3. every shard's moved rows into the local sums, read from the peers
+    void mp_delta(const std::vector<PeerView>& peers, const std::vector<cudaEvent_t>& moved_done,
+                  cudaEvent_t done) {
+        CK(cudaSetDevice(device_));
+        for (cudaEvent_t e : moved_done) CK(cudaStreamWaitEvent(stream_, e, 0));
+        for (const PeerView& q : peers)
+            launch(delta_local_kernel, grid_for(q.n * 32, 256), 256, q.indptr, q.idx, q.val, q.moved, q.n_moved, q.a,
+                   q.a_sum, static_cast<uint32_t*>(nullptr), S_.p, ld_, K_, touched_.p, Q_.p, nz_.p);
+        CK_LAUNCH();
+        CK(cudaEventRecord(done, stream_));
+    }
+
+    // 4. once every device has read this shard: the sums' owner map catches
+    // up, then the column rewrite and flags (identical on every device)
+    void mp_finish(const std::vector<cudaEvent_t>& delta_done, sskm_iteration_stats* st) {
+        CK(cudaSetDevice(device_));
+        for (cudaEvent_t e : delta_done) CK(cudaStreamWaitEvent(stream_, e, 0));
+        fill_sum_owner_local();
+        finish_update(st);
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        st->update_ms = ms;
+    }
+
+    // Rows `ids` (local) of the shard as host CSR (seed rows for a multi-device init).
+    void get_rows(const std::vector<uint32_t>& ids, std::vector<int64_t>& ptr, std::vector<int32_t>& idx,
+                  std::vector<float>& val) {
+        need_config();
+        CK(cudaSetDevice(device_));
+        const int64_t n = static_cast<int64_t>(ids.size());
+        ptr.assign(n + 1, 0);
+        idx.clear();
+        val.clear();
+        if (n == 0) return;
+        DevBuf<uint32_t> dids;
+        DevBuf<int64_t> lens, offs;
+        dids.alloc(n);
+        lens.alloc(n + 1);
+        offs.alloc(n + 1);
+        CK(cudaMemcpyAsync(dids.p, ids.data(), n * 4, cudaMemcpyHostToDevice, stream_));
+        launch(row_lens_kernel, grid_for(n + 1, 256), 256, dids.p, n, indptr_.p, lens.p);
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, lens.p, offs.p, static_cast<int>(n + 1), stream_));
+        DevBuf<unsigned char> tb;
+        tb.alloc(tmp);
+        CK(cub::DeviceScan::ExclusiveSum(tb.p, tmp, lens.p, offs.p, static_cast<int>(n + 1), stream_));
+        ++launches_;
+        CK(cudaMemcpyAsync(ptr.data(), offs.p, (n + 1) * 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        const int64_t nnz = ptr[n];
+        DevBuf<int32_t> di, dl;
+        DevBuf<float> dv;
+        di.alloc(std::max<int64_t>(nnz, 1));
+        dv.alloc(std::max<int64_t>(nnz, 1));
+        dl.alloc(n);
+        launch(pack_rows_kernel, grid_for(n * 32, 256), 256, dids.p, n, indptr_.p, idx_.p, val_.p, offs.p, dl.p, di.p,
+               dv.p);
+        CK_LAUNCH();
+        idx.resize(nnz);
+        val.resize(nnz);
+        if (nnz) {
+            CK(cudaMemcpyAsync(idx.data(), di.p, nnz * 4, cudaMemcpyDeviceToHost, stream_));
+            CK(cudaMemcpyAsync(val.data(), dv.p, nnz * 4, cudaMemcpyDeviceToHost, stream_));
+        }
+        CK(cudaStreamSynchronize(stream_));
     }
 
     // ------------------------------------------------------------ assign --
@@ -1983,17 +2108,31 @@ private:
 
 }  // namespace sskm_b200
 
+#include "multi.cuh"
+
 // ====================================================================== C-ABI
 using sskm_b200::Engine;
+using sskm_b200::MultiEngine;
 
 struct sskm_ctx {
     std::unique_ptr<Engine> eng;
 };
 
+struct sskm_multi {
+    std::unique_ptr<MultiEngine> m;
+};
+
 namespace {
 thread_local std::string g_err;
+// sskm_cluster_csr keeps one engine per device; the map lock is held only for
+// the lookup, each engine's own lock for its run (runs on different devices
+// proceed in parallel)
+struct CachedEngine {
+    std::mutex mu;
+    std::unique_ptr<Engine> eng;
+};
 std::mutex g_cache_mu;
-std::map<int, std::unique_ptr<Engine>> g_engine_cache;
+std::map<int, std::shared_ptr<CachedEngine>> g_engine_cache;
 
 template <class F>
 int guard(F&& f) {
@@ -2014,8 +2153,23 @@ int guard(F&& f) {
 
 Engine& E(sskm_ctx* c) {
     if (!c || !c->eng) throw sskm_b200::InvalidArgument("null context");
+    CK(cudaSetDevice(c->eng->device()));  // the calling thread may have another current device
     return *c->eng;
 }
+
+MultiEngine& M(sskm_multi* c) {
+    if (!c || !c->m) throw sskm_b200::InvalidArgument("null context");
+    return *c->m;
+}
+
+std::vector<int> device_list(int32_t n, const int32_t* devs) {
+    if (n <= 0 || !devs) throw sskm_b200::InvalidArgument("device list must not be empty");
+    return std::vector<int>(devs, devs + n);
+}
+
+template <class Step, class Cfg>
+void run_loop(Step&& step, const Cfg& cfg, sskm_iteration_stats* stats, uint32_t cap, uint32_t* n_iters,
+              int32_t* stop_reason, double* objective);
 
 bool stop_after(const sskm_iteration_stats& st, double conv, int32_t* reason) {
     if (st.n_reassigned == 0) {
@@ -2027,6 +2181,26 @@ bool stop_after(const sskm_iteration_stats& st, double conv, int32_t* reason) {
         return true;
     }
     return false;
+}
+
+// run() loop (engine.cpp:357-424) over any step function.
+template <class Step, class Cfg>
+void run_loop(Step&& step_fn, const Cfg& cfg, sskm_iteration_stats* stats, uint32_t cap, uint32_t* n_iters,
+              int32_t* stop_reason, double* objective) {
+    int32_t reason = SSKM_STOP_MAX_ITERATIONS;
+    uint32_t t = 0;
+    double obj = 0.0;
+    for (uint32_t iter = 1; iter <= cfg.max_iters; ++iter) {
+        sskm_iteration_stats st{};
+        step_fn(&st);
+        if (stats && t < cap) stats[t] = st;
+        ++t;
+        obj = st.objective;
+        if (stop_after(st, cfg.conv_sq_dist, &reason)) break;
+    }
+    if (n_iters) *n_iters = t;
+    if (stop_reason) *stop_reason = reason;
+    if (objective) *objective = obj;
 }
 
 void step(Engine& e, sskm_iteration_stats* st) {
@@ -2193,10 +2367,17 @@ int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims, 
         // one persistent engine per device: its HBM buffers are reused by the
         // next call instead of being freed (cudaFree synchronises and costs
         // ~0.1-0.5 s for the c1 working set)
-        std::lock_guard<std::mutex> lock(g_cache_mu);
-        auto& slot = g_engine_cache[cfg->device];
-        if (!slot) slot = std::make_unique<Engine>(cfg->device);
-        Engine& e = *slot;
+        std::shared_ptr<CachedEngine> slot;
+        {
+            std::lock_guard<std::mutex> lock(g_cache_mu);
+            auto& s = g_engine_cache[cfg->device];
+            if (!s) s = std::make_shared<CachedEngine>();
+            slot = s;
+        }
+        std::lock_guard<std::mutex> run_lock(slot->mu);
+        if (!slot->eng) slot->eng = std::make_unique<Engine>(cfg->device);
+        Engine& e = *slot->eng;
+        CK(cudaSetDevice(cfg->device));
         e.upload(n_docs, dims, indptr, indices, values, 0, n_docs);
         e.configure(*cfg);
         if (seeds) {
@@ -2220,6 +2401,86 @@ int sskm_cluster_csr(const sskm_run_config* cfg, int64_t n_docs, uint32_t dims, 
         if (n_iters) *n_iters = t;
         if (stop_reason) *stop_reason = reason;
         if (objective) *objective = obj;
+    });
+}
+
+// ------------------------------------------------------- multi-device --
+int sskm_multi_open(int32_t n_devices, const int32_t* devices, sskm_multi** out) {
+    return guard([&] {
+        if (!out) throw sskm_b200::InvalidArgument("null output");
+        auto* c = new sskm_multi();
+        try {
+            c->m = std::make_unique<MultiEngine>(device_list(n_devices, devices));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int sskm_multi_close(sskm_multi* ctx) {
+    return guard([&] { delete ctx; });
+}
+
+int sskm_multi_upload_csr(sskm_multi* ctx, int64_t n_docs, uint32_t dims, const int64_t* indptr,
+                          const int32_t* indices, const float* values) {
+    return guard([&] { M(ctx).upload(n_docs, dims, indptr, indices, values); });
+}
+
+int sskm_multi_configure(sskm_multi* ctx, const sskm_run_config* cfg) {
+    return guard([&] {
+        if (!cfg) throw sskm_b200::InvalidArgument("null config");
+        M(ctx).configure(*cfg);
+    });
+}
+
+int sskm_multi_init_from_seeds(sskm_multi* ctx, const uint32_t* seeds) {
+    return guard([&] { M(ctx).init_from_seeds(seeds); });
+}
+
+int sskm_multi_step(sskm_multi* ctx, sskm_iteration_stats* st) {
+    return guard([&] { M(ctx).step(st); });
+}
+
+int sskm_multi_run(sskm_multi* ctx, sskm_iteration_stats* stats, uint32_t cap, uint32_t* n_iters,
+                   int32_t* stop_reason) {
+    return guard([&] {
+        MultiEngine& m = M(ctx);
+        run_loop([&](sskm_iteration_stats* st) { m.step(st); }, m.config(), stats, cap, n_iters, stop_reason,
+                 nullptr);
+    });
+}
+
+int sskm_multi_get_state(sskm_multi* ctx, uint32_t* assignments, double* sims) {
+    return guard([&] { M(ctx).get_state(assignments, sims); });
+}
+
+int sskm_multi_get_centroids(sskm_multi* ctx, float* ct) {
+    return guard([&] { M(ctx).get_centroids(ct); });
+}
+
+int sskm_multi_launch_count(sskm_multi* ctx, uint64_t* n) {
+    return guard([&] { *n = M(ctx).launches(); });
+}
+
+int sskm_cluster_csr_multi(const sskm_run_config* cfg, int32_t n_devices, const int32_t* devices, int64_t n_docs,
+                           uint32_t dims, const int64_t* indptr, const int32_t* indices, const float* values,
+                           const uint32_t* seeds, uint32_t* assignments, double* sims, float* ct,
+                           sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters, int32_t* stop_reason,
+                           double* objective) {
+    return guard([&] {
+        if (!cfg) throw sskm_b200::InvalidArgument("null config");
+        Engine::validate(*cfg, n_docs > 0 ? static_cast<uint64_t>(n_docs) : 0);
+        if (!seeds) throw sskm_b200::InvalidArgument("a multi-device run needs init_seeds (k-means++ runs on one device)");
+        MultiEngine m(device_list(n_devices, devices));
+        m.upload(n_docs, dims, indptr, indices, values);
+        m.configure(*cfg);
+        m.init_from_seeds(seeds);
+        run_loop([&](sskm_iteration_stats* st) { m.step(st); }, *cfg, stats, stats_cap, n_iters, stop_reason,
+                 objective);
+        m.get_state(assignments, sims);
+        if (ct) m.get_centroids(ct);
     });
 }
 

@@ -117,12 +117,16 @@ __device__ __forceinline__ void atomic_add128(unsigned long long* q, __int128 v)
     atomicAdd(q + 1, hi + (old + lo < old ? 1ull : 0ull));
 }
 
-// Apply the rows of locally moved documents: warp per document, lanes over its
+// Apply the rows of moved documents: warp per document, lanes over its
 // nonzeros (distinct terms, so no intra-row conflicts); integer atomics only.
+// The document arrays (CSR, moved list, a, a_sum) may be a PEER device's shard,
+// read over NVLink (multi-device contexts: every device applies every shard's
+// moved rows to its own sums, no gather); a_sum_out (the local shard only, else
+// nullptr) records the cluster each row is now summed into.
 __global__ void delta_local_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
                                    const float* __restrict__ val, const uint32_t* __restrict__ moved,
                                    const unsigned long long* n_moved_p, const uint32_t* __restrict__ a,
-                                   uint32_t* __restrict__ a_sum, long long* __restrict__ S,
+                                   const uint32_t* a_sum, uint32_t* a_sum_out, long long* __restrict__ S,
                                    uint64_t ld, int K, uint8_t* __restrict__ touched,
                                    unsigned long long* __restrict__ Q, unsigned int* __restrict__ nz) {
     const int lane = threadIdx.x & (kWarp - 1);
@@ -149,7 +153,7 @@ __global__ void delta_local_kernel(const int64_t* __restrict__ indptr, const int
                 atomic_add128(Q + 2ull * oc, dold);
                 touched[oc] = 1;
             }
-            a_sum[i] = nc;
+            if (a_sum_out) a_sum_out[i] = nc;
         }
     }
 }
@@ -205,6 +209,13 @@ __global__ void moved_meta_kernel(const uint32_t* __restrict__ moved, const unsi
         old_c[m] = a_sum[i];
         new_c[m] = a[i];
     }
+}
+
+__global__ void row_lens_kernel(const uint32_t* __restrict__ ids, int64_t n, const int64_t* __restrict__ indptr,
+                                int64_t* __restrict__ lens) {
+    for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m <= n;
+         m += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        lens[m] = m == n ? 0 : indptr[ids[m] + 1] - indptr[ids[m]];
 }
 
 __global__ void pack_rows_kernel(const uint32_t* __restrict__ moved, int64_t n_moved,
