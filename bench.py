@@ -379,6 +379,11 @@ def run_ours(args):
                      "assign": statistics.mean(s.assign_ms for s in stats),
                      "assign_kernels": statistics.mean(s.assign_kernel_ms for s in stats),
                      "screen": roofline["screen_ms_per_assign"]},
+        "drift_bound": {"docs_kept_per_iter": statistics.mean(s.skip_docs for s in stats),
+                        "ms": statistics.mean(s.skip_ms for s in stats),
+                        "last_5_docs_kept": statistics.mean(s.skip_docs for s in stats[-5:]),
+                        "note": "documents the drift bound kept in their cluster without a screen "
+                                "(drift bound pass, DESIGN.md §3.1b)"},
         "moved_per_iter": statistics.mean(s.n_moved for s in stats),
         "exact_scan_docs_per_iter": statistics.mean(s.n_exact for s in stats),
         "roofline": roofline,

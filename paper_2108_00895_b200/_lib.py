@@ -68,6 +68,10 @@ class sskm_iteration_stats(C.Structure):
         ("bound_theta", C.c_double),
         ("bound_visits", C.c_uint64),
         ("bound_own_dots", C.c_uint64),
+        ("skip_docs", C.c_uint64),
+        ("reserved1", C.c_uint64),
+        ("reserved2", C.c_uint64),
+        ("skip_ms", C.c_double),
     ]
 
 

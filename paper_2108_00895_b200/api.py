@@ -127,6 +127,10 @@ class IterationStats:
     bound_theta: float = 0.0
     bound_visits: int = 0
     bound_own_dots: int = 0
+    skip_docs: int = 0
+    reserved1: int = 0
+    reserved2: int = 0
+    skip_ms: float = 0.0
 
     @classmethod
     def from_c(cls, s: sskm_iteration_stats) -> "IterationStats":

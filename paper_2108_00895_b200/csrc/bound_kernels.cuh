@@ -58,6 +58,7 @@ struct BoundArgs {
     uint32_t k;
     int first;                 // first tile: establish the baseline and decide take
     int single_tile;           // the tile holds every column (its low maxima bound every cluster)
+    int last;                  // last tile of the pass
     const unsigned long long* hp_overflow;  // the postings build dropped lists (then only Σ|x|·L_t bounds)
     uint32_t* a;               // in/out: running exact argmax
     double* sims;              // in/out: running exact max
@@ -74,6 +75,13 @@ struct BoundArgs {
     unsigned long long* n_visits;    // documents visited, summed over tiles (roofline bytes)
     unsigned long long* n_cand_nnz;  // nonzeros of the candidate dots (centroid values gathered)
     unsigned long long* n_own;       // own dots computed in the screen
+    // drift bound (single-tile full-scan passes; nullptr otherwise): per
+    // document a certified upper bound on its similarity to every cluster other
+    // than its own, and the iteration it holds for (skip_kernel)
+    float* ub;
+    uint32_t* ub_it;
+    uint32_t iter;
+    const unsigned long long* n_work_dev;  // work-list length on the device (overrides n_work)
 };
 
 // Per-warp shared memory of the bound screen (bytes).
@@ -197,14 +205,19 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     double* fold = reinterpret_cast<double*>(base + SM::o_fold);
     const uint32_t s_acc = sb + SM::o_acc, s_tl = sb + SM::o_tl, s_cnt = sb + SM::o_cnt, s_st = sb + SM::o_stats;
     for (int c = lane; c < KT; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
-    if (lane < 8) sm_st_u32(s_st + 4u * lane, 0u);
+    if (lane < 7) sm_st_u32(s_st + 4u * lane, 0u);
     __syncwarp();
     const uint2* __restrict__ pairs = p.pairs;
     const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-    const uint32_t n_work = static_cast<uint32_t>(p.n_work);
+    // the block's work range; with a device-side list length (drift-bound work
+    // list) its end lives in the warp's statistics slot 7, re-read where used
+    // (a register would have to survive the whole pipeline)
+    const uint32_t n_work = static_cast<uint32_t>(p.n_work_dev ? *p.n_work_dev : p.n_work);
     const uint32_t chunk = static_cast<uint32_t>(ceil_div(n_work, gridDim.x));
     const uint32_t w0 = blockIdx.x * chunk;
-    const uint32_t w1 = min(n_work, w0 + chunk);
+    if (lane == 0) sm_st_u32(s_st + 28u, min(n_work, w0 + chunk));
+    __syncwarp();
+#define w1 sm_ld_u32(s_st + 28u)
     const bool first = p.first != 0;
     const bool hp_ovf = *p.hp_overflow != 0;
     const uint32_t* __restrict__ indptr = reinterpret_cast<const uint32_t*>(p.indptr32);
@@ -346,9 +359,13 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     uint2 pa, pb;
                     float xa, xb2;
                     slot(wb + lane, pa, xa);
-                    slot(wb + kWarp + lane, pb, xb2);
-                    accumulate(pa, xa);
-                    accumulate(pb, xb2);
+                    if (wb + kWarp < total) {  // a second window only when there are pairs for it
+                        slot(wb + kWarp + lane, pb, xb2);
+                        accumulate(pa, xa);
+                        accumulate(pb, xb2);
+                    } else {
+                        accumulate(pa, xa);
+                    }
                 }
                 // the next chunk's extents, now that its terms have arrived: in
                 // flight during this chunk's fold and the loop turn
@@ -411,6 +428,15 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             const double bx = lowb + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
             // no touched cluster can reach best: nothing to evaluate
             const uint32_t count = static_cast<double>(accmax) * kFixUnit + bx >= best ? (dense ? p.kt : ntouch) : 0u;
+            if (p.ub && lane == 0) {
+                // every other cluster j of this tile: s_j <= acc_j·2^-30 + bx <=
+                // accmax·2^-30 + bx (the own cluster's pairs were never
+                // accumulated); the maximum over the tiles; withdrawn below if
+                // the document moves (its new cluster's pairs were)
+                const float u = __double2float_ru(static_cast<double>(accmax) * kFixUnit + bx);
+                p.ub[i] = first ? u : fmaxf(p.ub[i], u);
+                if (first) p.ub_it[i] = p.iter;
+            }
             uint32_t c_gid = 0;   // this lane's pending candidate
             double c_ub = -1e300;
             bool c_on = false;
@@ -483,9 +509,12 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             }
             drain(true);
             if (lane == 0) {
+                if (p.ub && p.last && arg != p.a_start[i]) p.ub[i] = __int_as_float(0x7f800000);
                 p.a[i] = arg;
                 p.sims[i] = best;
             }
+        } else if (first && p.ub && lane == 0) {
+            p.ub[i] = __int_as_float(0x7f800000);  // exact scan: no bound
         }
         // clear the touched accumulators
         __syncwarp();
@@ -504,6 +533,96 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         atomicAdd(p.n_cand, static_cast<unsigned long long>(sm_ld_u32(s_st + 16)));
         atomicAdd(p.n_cand_nnz, static_cast<unsigned long long>(sm_ld_u32(s_st + 20)));
     }
+#undef w1
+}
+
+// Drift bound (full-scan passes). The bound screen leaves, for every document
+// that kept its cluster a, U_i >= s_ij for every j != a: the reference's fp64
+// dot against the centroids of that iteration t_s. Centroid columns then move
+// by δ_j = ||c_j^new − c_j^old||_2 per update, so in real arithmetic x·c_j grows
+// by at most ||x||_2·Σδ, and
+//   s_ij(t) <= U_i + ||x||_2·(D(t) − D(t_s)) + 2·γ64(n)·||x||_2·cmax,
+// D = the running sum of the updates' max_j δ_j (the two γ64 terms convert
+// between the reference's rounded dots and real ones at t_s and at t). A
+// document whose own column is bit-identical to the previous iteration's
+// (`same`: its cached similarity is exact) and whose cached own similarity
+// exceeds that bound strictly keeps its cluster with exactly the reference's
+// result — no other cluster can win or tie — and needs no screen. Every other
+// document goes to a work list for the bound screen, ascending within each
+// block's 1024-document range. (Documents whose own column moved need an own
+// dot in any case; the screen computes it fused with its loads, far cheaper
+// than a separate pass — measured.) The paper's use of centroid stability
+// (unchanged clusters, engine.cpp:268-275) is the ε = 0 case of this bound.
+struct SkipArgs {
+    const int64_t* indptr;
+    int64_t n;
+    const uint32_t* a;
+    const double* sims;
+    const uint8_t* same;
+    const float* ub;
+    const uint32_t* ub_it;
+    const double* dcum;  // D by iteration
+    uint32_t iter;
+    const float2* xb;
+    double cmax;
+    uint32_t* list;
+    unsigned long long* n_list;
+    unsigned long long* n_kept;  // documents kept out of the screen
+};
+
+constexpr int kSkipDocsPerBlock = 1024;
+
+__global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
+    __shared__ uint32_t wsum[8];
+    __shared__ unsigned long long base_sm;
+    const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
+    const int64_t d0 = static_cast<int64_t>(blockIdx.x) * kSkipDocsPerBlock;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(kSkipDocsPerBlock), p.n - d0));
+    constexpr int kPer = kSkipDocsPerBlock / 256;
+    const int my0 = threadIdx.x * kPer;  // four consecutive documents per thread
+    const double dnow = p.dcum[p.iter];
+    bool kp[kPer];
+    uint32_t mine = 0, out = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        kp[q] = false;
+        if (my0 + q >= cnt) continue;
+        const int64_t i = d0 + my0 + q;
+        kp[q] = true;
+        const float u = p.ub[i];
+        if (u != __int_as_float(0x7f800000) && p.same[p.a[i]]) {
+            const float2 xb = p.xb[i];
+            const double nn = static_cast<double>(p.indptr[i + 1] - p.indptr[i]);
+            const double grow = static_cast<double>(xb.y) * (dnow - p.dcum[p.ub_it[i]]) * (1.0 + 1e-9);
+            const double b = static_cast<double>(u) + grow + 2.0 * gamma_ub(nn, 0x1p-53) * xb.y * p.cmax * (1.0 + 1e-12) +
+                             nn * 0x1p-126;
+            kp[q] = !(p.sims[i] > b);
+        }
+        mine += kp[q];
+        out += !kp[q];
+    }
+    uint32_t incl = mine;
+#pragma unroll
+    for (int off = 1; off < kWarp; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += o;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) out += __shfl_xor_sync(0xFFFFFFFFu, out, off);
+    if (lane == kWarp - 1) wsum[warp] = incl;
+    if (lane == 0 && out) atomicAdd(p.n_kept, static_cast<unsigned long long>(out));
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (int w = 0; w < nwarps; ++w) {
+        if (w < warp) before += wsum[w];
+        total += wsum[w];
+    }
+    if (threadIdx.x == 0) base_sm = total ? atomicAdd(p.n_list, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
+    unsigned long long o = base_sm + before + (incl - mine);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+        if (kp[q]) p.list[o++] = static_cast<uint32_t>(d0 + my0 + q);
 }
 
 // High postings of the cluster tile [c0, c0 + kt) of M in one pass over M:

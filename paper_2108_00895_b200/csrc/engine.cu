@@ -88,6 +88,7 @@ public:
         if (const char* e = std::getenv("SSKM_NCC_FULL_FRAC")) ncc_full_frac_ = std::atof(e);
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_DEBUG")) debug_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_THETA")) {
             theta_ = static_cast<float>(std::atof(e));
@@ -200,6 +201,7 @@ public:
         // must not leave a context whose sizes disagree with its buffers
         corpus_ = false;
         state_ = false;
+        ub_valid_ = false;
         k_ = 0;
         if (n <= 0) throw InvalidArgument("empty corpus");
         if (dims == 0) throw InvalidArgument("dims must be positive");
@@ -432,6 +434,7 @@ public:
         seed_cmax(dseeds.p);
         reset_sums();
         CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
+        ub_valid_ = false;
         iteration_ = 0;
         have_cc_ = false;
         state_ = true;
@@ -839,6 +842,7 @@ public:
         } else {
             scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, order, n_);
         }
+        if (!bound_active()) ub_valid_ = false;
         CK(cudaEventRecord(ev_[5], stream_));
         finish_assign(st);
         cache_trusted_ = true;
@@ -907,6 +911,7 @@ public:
             }
         }
         CK(cudaEventRecord(ev_[5], stream_));
+        if (!(n_chg_ > 0 && full_equiv)) ub_valid_ = false;  // per-document bounds not refreshed for every document
         last_full_equiv_ = n_chg_ > 0 && full_equiv;
         last_n_rescan_ = n_rescan;
         finish_assign(st);
@@ -950,6 +955,7 @@ public:
         if (sims) CK(cudaMemcpyAsync(sims_.p, sims, n_ * 8, cudaMemcpyHostToDevice, stream_));
         iteration_ = iteration;
         cache_trusted_ = false;  // externally supplied cache: follow the reference's NCC literally
+        ub_valid_ = false;
         CK(cudaStreamSynchronize(stream_));
     }
 
@@ -1018,6 +1024,7 @@ public:
         reset_sums();
         have_cc_ = false;
         cache_trusted_ = false;
+        ub_valid_ = false;
         CK(cudaStreamSynchronize(stream_));
     }
 
@@ -1201,6 +1208,16 @@ private:
         pcnt_.alloc(d_ + 1);
         pptr_.alloc(d_ + 1);
         moves_.alloc(2 * static_cast<size_t>(k_));
+        // drift bound (skip_kernel)
+        ub_.alloc(n_);
+        ub_it_.alloc(n_);
+        skip_list_.alloc(n_);
+        skip_ctr_.alloc(4);
+        if (dcum_.n == 0) dcum_.alloc(4096);
+        btake_.alloc(n_);
+        bctr_.alloc(8);
+        hptr_.alloc(d_);
+        hpctr_.alloc(2);
         size_t t1 = 0, t2 = 0, t3 = 0;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys_.p, keys_.p + n_, vals_.p, vals_.p + n_,
                                            static_cast<int>(n_), 0, 64, stream_));
@@ -1229,6 +1246,7 @@ private:
     }
 
     void seed_assign_state() {
+        ub_valid_ = false;
         launch(fill_u32_kernel, grid_for(n_, 256), 256, a_.p, n_, 0);
         launch(fill_f64_kernel, grid_for(n_, 256), 256, sims_.p, n_, -2.0);
         CK_LAUNCH();
@@ -1350,7 +1368,7 @@ private:
         const uint32_t n_groups = static_cast<uint32_t>(ceil_div(k_, 32));
         launch(write_groups_kernel, dim3(static_cast<unsigned>(ceil_div(n_groups, 4)), n_rb), 128, S_.p, ct_.p,
                (uint64_t)ld_, d_, k_, touched_.p, Q_.p, part_.p, &scal_.p->zero_flag, nz_.p);
-        launch(reduce_groups_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 256, part_.p, n_rb, k_, touched_.p,
+        launch(reduce_groups_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 1024, part_.p, n_rb, k_, touched_.p,
                drift_.p, &scal_.p->n_rec);
         launch(flags_kernel, grid_for(k_, 256), 256, k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon,
                repaired_flag_.p, drift_.p, unchanged_.p, same_.p, &scal_.p->max_drift_bits,
@@ -1367,6 +1385,7 @@ private:
         if (n_rec > 0) cmax_ = (n_rec == k_) ? 1.0 + 0x1p-22 : std::max(cmax_, 1.0 + 0x1p-22);
         double max_drift;
         std::memcpy(&max_drift, &hs_->max_drift_bits, 8);
+        advance_drift(max_drift);
         have_cc_ = false;
         std::memset(st, 0, sizeof(*st));
         st->iteration = iteration_;
@@ -1375,6 +1394,27 @@ private:
         st->n_repaired = static_cast<int32_t>(repaired_.size());
         st->n_moved = hs_->n_moved;
         st->n_recomputed = n_rec;
+    }
+
+    // Running sum D of the updates' max column drift (the drift bound's growth,
+    // skip_kernel); an update the bounds cannot follow (iteration 1, an
+    // empty-cluster repair) invalidates them until the next full screen.
+    void advance_drift(double max_sq_drift) {
+        if (dcum_h_.empty()) dcum_h_.push_back(0.0);
+        while (dcum_h_.size() <= iteration_) dcum_h_.push_back(dcum_h_.back());
+        const bool ok = iteration_ >= 2 && repaired_.empty() && max_sq_drift >= 0.0 && std::isfinite(max_sq_drift);
+        const double step = ok ? std::sqrt(max_sq_drift) * (1.0 + 1e-9) : 0.0;
+        dcum_h_[iteration_] = (iteration_ > 0 ? dcum_h_[iteration_ - 1] : 0.0) + step;
+        if (!ok) ub_valid_ = false;
+        if (dcum_.n < dcum_h_.size()) {
+            dcum_.alloc(std::max<size_t>(4096, 2 * dcum_h_.size()));
+            CK(cudaMemcpyAsync(dcum_.p, dcum_h_.data(), dcum_h_.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               stream_));
+        } else {
+            CK(cudaMemcpyAsync(dcum_.p + iteration_, &dcum_h_[iteration_], sizeof(double), cudaMemcpyHostToDevice,
+                               stream_));
+        }
+        CK(cudaStreamSynchronize(stream_));  // the host vector may reallocate before the next copy
     }
 
     void ensure_cc() {
@@ -1399,6 +1439,8 @@ private:
         bstat_docs_ = bstat_pairs_ = bstat_cand_ = bstat_doc_nnz_ = bstat_cand_nnz_ = bstat_visits_ = bstat_own_ = 0;
         bstat_theta_ = 0.0;
         dots_ = 0;
+        skip_docs_ = 0;
+        skip_ms_ = 0.0;
         CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
         CK(cudaMemcpyAsync(sims_start_.p, sims_.p, n_ * 8, cudaMemcpyDeviceToDevice, stream_));
     }
@@ -1514,6 +1556,45 @@ private:
         p.n_own = bctr_.p + 3;
         p.n_doc_nnz = bctr_.p + 4;
         p.n_cand_nnz = bctr_.p + 5;
+        // drift bound: single-tile full-scan passes over every document refresh
+        // the per-document bounds; with valid bounds, a pre-pass first keeps
+        // the documents that provably keep their cluster (skip_kernel)
+        const bool full_cover = init == kInitFull && order == nullptr && col_ids == nullptr && n_work == n_;
+        bool skipped = false;
+        if (full_cover) {
+            ub_.alloc(n_);
+            ub_it_.alloc(n_);
+            p.ub = ub_.p;
+            p.ub_it = ub_it_.p;
+            p.iter = iteration_;
+            if (skip_enabled_ && ub_valid_ && p.same && iteration_ < dcum_h_.size()) {
+                skip_list_.alloc(n_);
+                skip_ctr_.alloc(4);
+                CK(cudaMemsetAsync(skip_ctr_.p, 0, 4 * sizeof(unsigned long long), stream_));
+                SkipArgs q{};
+                q.indptr = indptr_.p;
+                q.n = n_;
+                q.a = a_.p;
+                q.sims = sims_.p;
+                q.same = p.same;
+                q.ub = ub_.p;
+                q.ub_it = ub_it_.p;
+                q.dcum = dcum_.p;
+                q.iter = iteration_;
+                q.xb = xb_.p;
+                q.cmax = cmax_;
+                q.list = skip_list_.p;
+                q.n_list = skip_ctr_.p;
+                q.n_kept = skip_ctr_.p + 1;
+                CK(cudaEventRecord(ev_[10], stream_));
+                launch(skip_kernel, static_cast<unsigned>(ceil_div(n_, kSkipDocsPerBlock)), 256, q);
+                CK(cudaEventRecord(ev_[11], stream_));
+                CK_LAUNCH();
+                p.order = skip_list_.p;
+                p.n_work_dev = skip_ctr_.p;
+                skipped = true;
+            }
+        }
         if (col_ids) {  // cluster -> column of M
             bcol_of_.alloc(k_);
             launch(fill_u32_kernel, grid_for(k_, 256), 256, bcol_of_.p, static_cast<int64_t>(k_), kNone);
@@ -1537,6 +1618,7 @@ private:
             p.kt = kt;
             p.first = c0 == 0 ? 1 : 0;
             p.single_tile = ncols <= KT ? 1 : 0;
+            p.last = c0 + KT >= ncols ? 1 : 0;
             p.hp_overflow = hpctr_.p + 1;
             // the screen launches are timed as one interval: the event pair
             // brackets every tile's screen, and the postings builds between
@@ -1554,11 +1636,20 @@ private:
                    sims_start_.p, sims_.p, unchanged_.p, rescan_.p, &scal_.p->n_rescan);
         // θ for the next assign: keep the exact-scan share small and the
         // candidate dots near one per document (θ never changes a result)
-        unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0}, hp[2] = {0, 0};
+        unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0}, hp[2] = {0, 0}, sk[4] = {0, 0, 0, 0};
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hp, hpctr_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
+        if (skipped) CK(cudaMemcpyAsync(sk, skip_ctr_.p, sizeof(sk), cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
+        if (full_cover) ub_valid_ = true;  // every document: screened (fresh bound) or kept (bound still valid)
+        if (skipped) {
+            n_work = static_cast<int64_t>(sk[0]);  // the screen's work list
+            skip_docs_ += sk[1];
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_[10], ev_[11]));
+            skip_ms_ += ms;
+        }
         scalars_fresh_ = true;
         if (hp[0] > pairs_.n) grow_pairs(hp[0]);  // the last tile's lists overflowed: room for the next pass
         last_hp_overflow_ = hp[1] != 0;
@@ -2001,12 +2092,14 @@ private:
         st->bound_theta = bstat_theta_;
         st->bound_visits = bstat_visits_;
         st->bound_own_dots = bstat_own_;
+        st->skip_docs = skip_docs_;
+        st->skip_ms = skip_ms_;
     }
 
     int device_;
     int sms_ = 148;
     cudaStream_t stream_{};
-    cudaEvent_t ev_[10]{};
+    cudaEvent_t ev_[12]{};
     static constexpr int kUserEvents = 256;
     cudaEvent_t user_ev_[kUserEvents]{};
     uint64_t launches_ = 0;
@@ -2087,7 +2180,17 @@ private:
              bstat_visits_ = 0, bstat_own_ = 0;
     uint32_t updates_since_assign_ = 0;  // updates since the last assign (the same_ flags' validity)
     double bstat_theta_ = 0.0;
-    uint64_t dots_ = 0;  // dots the kernels evaluated in the current assign (gpu_dot_products)
+    uint64_t dots_ = 0;
+    // drift bound (skip_kernel)
+    DevBuf<float> ub_;
+    DevBuf<uint32_t> ub_it_, skip_list_;
+    DevBuf<double> dcum_;
+    DevBuf<unsigned long long> skip_ctr_;
+    std::vector<double> dcum_h_;
+    bool ub_valid_ = false;     // every document's bound is valid for the current assignments
+    bool skip_enabled_ = true;  // SSKM_SKIP=0: screen every document
+    uint64_t skip_docs_ = 0;
+    double skip_ms_ = 0.0;  // dots the kernels evaluated in the current assign (gpu_dot_products)
     bool nonneg_ = true;
     double last_density_ = 0.0;
     double dense_above_ = 0.15;
@@ -2232,6 +2335,8 @@ void step(Engine& e, sskm_iteration_stats* st) {
     st->bound_theta = a.bound_theta;
     st->bound_visits = a.bound_visits;
     st->bound_own_dots = a.bound_own_dots;
+    st->skip_docs = a.skip_docs;
+    st->skip_ms = a.skip_ms;
     st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 }  // namespace

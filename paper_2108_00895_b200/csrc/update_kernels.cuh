@@ -357,26 +357,39 @@ __global__ void __launch_bounds__(128) write_groups_kernel(const long long* __re
 }
 
 // Per touched column: the row-block partials of write_groups_kernel summed in a
-// fixed association (8 segments of row blocks in order, then the 8 segment sums
-// in order: deterministic); the count of touched columns.
-__global__ void __launch_bounds__(256) reduce_groups_kernel(const double* __restrict__ part, uint32_t n_rb, uint32_t k,
-                                                            const uint8_t* __restrict__ touched,
-                                                            double* __restrict__ drift, unsigned int* n_rec) {
-    __shared__ double sh[8][32];
+// fixed association (32 segments of row blocks, each summed in order, then the
+// 32 segment sums in order: deterministic); the count of touched columns.
+// 1024 threads = 32 columns × 32 segments.
+__global__ void __launch_bounds__(1024) reduce_groups_kernel(const double* __restrict__ part, uint32_t n_rb, uint32_t k,
+                                                             const uint8_t* __restrict__ touched,
+                                                             double* __restrict__ drift, unsigned int* n_rec) {
+    __shared__ double sh[32][33];
     const uint32_t cl = threadIdx.x & 31, seg = threadIdx.x >> 5;
     const uint32_t c = blockIdx.x * 32 + cl;
     const bool on = c < k && touched[c] != 0;
-    const uint32_t per = (n_rb + 7) / 8;
+    const uint32_t per = (n_rb + 31) / 32;
+    const uint32_t r0 = seg * per, r1 = min(n_rb, r0 + per);
     double s = 0.0;
-    if (on)
-        for (uint32_t rb = seg * per; rb < min(n_rb, (seg + 1) * per); ++rb) s += part[static_cast<uint64_t>(rb) * k + c];
+    if (on) {
+        uint32_t rb = r0;
+        for (; rb + 4 <= r1; rb += 4) {  // loads first, then the in-order adds
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = part[static_cast<uint64_t>(rb + q) * k + c];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s += v[q];
+        }
+        for (; rb < r1; ++rb) s += part[static_cast<uint64_t>(rb) * k + c];
+    }
     sh[seg][cl] = s;
     __syncthreads();
     if (seg == 0 && c < k) {
         double t = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t += sh[q][cl];
+        for (int q = 0; q < 32; ++q) t += sh[q][cl];
         drift[c] = on ? t : 0.0;
+    }
+    if (seg == 0) {
         const unsigned b = __ballot_sync(0xFFFFFFFFu, on);
         if (cl == 0 && b) atomicAdd(n_rec, static_cast<unsigned>(__popc(b)));
     }

@@ -10,6 +10,7 @@ from paper_2108_00895_b200 import synthetic as S
 
 cfg = S.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c1"]
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+stats_only = "--stats-only" in sys.argv
 data = S.corpus(cfg)
 k = cfg.k
 eng = P.Engine(0)
@@ -17,17 +18,24 @@ eng.upload(data)
 eng.configure(k, mode="baseline", conv_sq_dist=1e-300, max_iters=10**6)
 eng.init_from_seeds(S.init_seeds(data.n_docs, k, 0))
 rng = np.random.default_rng(3)
-docs = np.sort(rng.choice(data.n_docs, 4000, replace=False))
-X = np.zeros((len(docs), data.dims), np.float32)
+docs = np.sort(rng.choice(data.n_docs, 4000 if not stats_only else 1, replace=False))
+X = np.zeros((len(docs), data.dims if not stats_only else 1), np.float32)
 xn = np.zeros(len(docs))
-for q, i in enumerate(docs):
+for q, i in enumerate(docs if not stats_only else []):
     b, e = data.indptr[i], data.indptr[i + 1]
     X[q, data.indices[b:e]] = data.values[b:e]
     xn[q] = np.linalg.norm(data.values[b:e].astype(np.float64))
-prev = eng.get_centroids()
+prev = eng.get_centroids() if not stats_only else None
 for it in range(1, iters + 1):
     t0 = time.perf_counter()
     st = eng.step()
+    if stats_only:
+        print(json.dumps({"it": it, "ms": st.update_ms + st.assign_ms, "upd": st.update_ms, "asg": st.assign_ms,
+                          "screen": st.screen_ms, "theta": st.bound_theta, "moved": st.n_moved, "own": st.bound_own_dots,
+                          "reassigned": st.n_reassigned, "recomputed": st.n_recomputed, "exact": st.n_exact,
+                          "skip_docs": st.skip_docs, "skip_ms": st.skip_ms,
+                          "launches": st.screen_launches, "wall": time.perf_counter() - t0}), flush=True)
+        continue
     ct = eng.get_centroids()
     d = np.sqrt(((ct.astype(np.float64) - prev) ** 2).sum(0))
     prev = ct.astype(np.float64)
@@ -41,7 +49,7 @@ for it in range(1, iters + 1):
     out = {"it": it, "ms": st.update_ms + st.assign_ms, "upd": st.update_ms, "asg": st.assign_ms, "screen": st.screen_ms,
            "theta": st.bound_theta, "pairs_per_doc": st.bound_pairs / data.n_docs,
            "cand_per_doc": st.bound_candidates / data.n_docs, "own": st.bound_own_dots, "moved": st.n_moved,
-           "reassigned": st.n_reassigned, "recomputed": st.n_recomputed, "exact": st.n_exact,
+           "reassigned": st.n_reassigned, "skip_docs": st.skip_docs, "skip_ms": st.skip_ms, "recomputed": st.n_recomputed, "exact": st.n_exact,
            "drift_max": float(dmax), "drift_q50_90_99": [float(x) for x in q],
            "gap_q10_50": [float(x) for x in np.quantile(gap, [0.1, 0.5])], "skip_frac_dmax": float(skip1)}
     for qq in (0.5, 0.9, 0.99):

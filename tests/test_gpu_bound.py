@@ -112,3 +112,35 @@ def test_postings_overflow_stays_exact(case, monkeypatch):
     monkeypatch.setenv("SSKM_PAIRS_CAP", "64")
     t, _ = trajectory(m, k, seeds, "baseline", 4)
     assert_same(ref, t, "pairs cap 64")
+
+
+@pytest.mark.parametrize("case", ["one_tile", "two_tiles", "signed"])
+def test_drift_bound_skip_is_exact(case, monkeypatch):
+    """Documents kept in their cluster by the drift bound (skip_test_kernel)
+    must leave exactly the trajectory of screening every document
+    (SSKM_SKIP=0), and the bound must actually keep documents once the
+    centroids settle."""
+    m, k = CASES[case]()
+    seeds = S.init_seeds(m.n_docs, k, 0)
+    iters = 16
+
+    def run():
+        eng = P.Engine(0)
+        eng.upload(m)
+        eng.configure(k, mode="baseline", conv_sq_dist=1e-300, max_iters=iters)
+        eng.init_from_seeds(seeds)
+        out, skipped = [], 0
+        for _ in range(iters):
+            st = eng.step()
+            a, s, _ = eng.get_state()
+            out.append((a.copy(), s.copy(), st.dot_products, st.n_reassigned))
+            skipped += st.skip_docs
+        return out, skipped
+
+    monkeypatch.setenv("SSKM_SKIP", "0")
+    ref, s0 = run()
+    monkeypatch.setenv("SSKM_SKIP", "1")
+    got, s1 = run()
+    assert s0 == 0
+    assert s1 > 0
+    assert_same(ref, got, f"skip {case}")
