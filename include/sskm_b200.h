@@ -193,6 +193,11 @@ int sskm_cluster_csr_multi(const sskm_run_config* cfg, int32_t n_devices, const 
                            sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters,
                            int32_t* stop_reason, double* objective);
 
+/* Test hook: rebuilds the bound screen's high postings from the current
+ * centroids and compares them with the lists kept and maintained in place
+ * across iterations; bad_rows = differing rows, -1 when none are kept. */
+int sskm_debug_check_postings(sskm_ctx* ctx, int64_t* bad_rows);
+
 /* Device timing on the context's stream (CUDA events; 256 slots) and the
  * number of kernels this context has launched — the bench's live evidence. */
 int sskm_timer_record(sskm_ctx* ctx, int32_t slot);

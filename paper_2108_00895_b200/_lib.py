@@ -105,6 +105,7 @@ SIGNATURES = [
     ("sskm_get_centroid_rows", C.c_int, [_P, C.c_uint32, _u32p, _f32p]),
     ("sskm_get_centroid_cols", C.c_int, [_P, C.c_uint32, _u32p, _f32p]),
     ("sskm_set_centroids", C.c_int, [_P, _f32p]),
+    ("sskm_debug_check_postings", C.c_int, [_P, C.POINTER(C.c_int64)]),
     ("sskm_get_repaired", C.c_int, [_P, _u32p, C.POINTER(C.c_uint32)]),
     ("sskm_get_iteration", C.c_int, [_P, C.POINTER(C.c_uint32)]),
     ("sskm_cluster_csr", C.c_int, [_CFG, C.c_int64, C.c_uint32, _i64p, _i32p, _f32p, _P, _P, _P, _P,

@@ -299,6 +299,12 @@ class Engine:
             check(self.lib.sskm_get_centroid_cols(self.h, len(cols), cols, out))
         return out
 
+    def debug_check_postings(self) -> int:
+        """Rows where the kept high postings differ from a fresh build (-1: none kept)."""
+        n = C.c_int64()
+        check(self.lib.sskm_debug_check_postings(self.h, C.byref(n)))
+        return int(n.value)
+
     def set_centroids(self, ct: np.ndarray):
         ct = np.ascontiguousarray(ct, np.float32)
         if ct.shape != (self.dims, self.k):

@@ -82,14 +82,20 @@ struct BoundArgs {
     uint32_t* ub_it;
     uint32_t iter;
     const unsigned long long* n_work_dev;  // work-list length on the device (overrides n_work)
+    unsigned long long* n_hovf;      // documents whose hash table overflowed (HT > 0)
 };
 
-// Per-warp shared memory of the bound screen (bytes).
-template <int KT>
+// Per-warp shared memory of the bound screen (bytes). HT > 0: the
+// accumulators are a hash table of HT slots keyed by column (one pass over
+// every column, however many: configs 2 and 4), else KT slots, one per column
+// of a cluster tile.
+template <int KT, int HT = 0>
 struct BoundSmem {
-    static constexpr int kCap = 256;  // touched clusters tracked before a dense sweep of the tile
-    static constexpr uint32_t o_acc = 0;                   // int32[KT] fixed-point accumulators
-    static constexpr uint32_t o_fold = o_acc + KT * 4;     // double[32] fold buffer
+    static constexpr int kCap = 256;  // touched slots tracked before a dense sweep of the table
+    static constexpr int kSlots = HT > 0 ? HT : KT;
+    static constexpr uint32_t o_acc = 0;                          // int32[kSlots] fixed-point accumulators
+    static constexpr uint32_t o_key = o_acc + kSlots * 4;         // u32[HT] hash keys: column + 1 (0 = empty)
+    static constexpr uint32_t o_fold = o_key + (HT > 0 ? HT * 4 : 0);  // double[32] fold buffer
     static constexpr uint32_t o_tl = o_fold + 32 * 8;      // u16[kCap] touched list
     static constexpr uint32_t o_cnt = o_tl + kCap * 2;     // u32 touched count
     static constexpr uint32_t o_stats = o_cnt + 16;        // u32[8] per-warp statistics
@@ -113,6 +119,11 @@ __device__ __forceinline__ void sm_st_u16(uint32_t a, uint32_t v) {
 __device__ __forceinline__ int sm_atom_add(uint32_t a, int v) {
     int old;
     asm volatile("atom.shared.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
+    return old;
+}
+__device__ __forceinline__ uint32_t sm_atom_cas(uint32_t a, uint32_t cmp, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v));
     return old;
 }
 
@@ -193,10 +204,11 @@ __device__ __forceinline__ double gamma_ub(double n, double u) {
 // Offsets are 32-bit (the host requires nnz < 2^32 per device for this kernel)
 // and the statistics counters live in shared memory, to keep the pipelined
 // loads in registers.
-template <int KT, int INIT>
+template <int KT, int INIT, int HT = 0>
 __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(BoundArgs p) {
-    using SM = BoundSmem<KT>;
+    using SM = BoundSmem<KT, HT>;
     constexpr int kCap = SM::kCap;
+    constexpr int kSlots = SM::kSlots;
     extern __shared__ __align__(16) unsigned char smem_b[];
     const int lane = threadIdx.x & (kWarp - 1);
     const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
@@ -204,7 +216,10 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(base));
     double* fold = reinterpret_cast<double*>(base + SM::o_fold);
     const uint32_t s_acc = sb + SM::o_acc, s_tl = sb + SM::o_tl, s_cnt = sb + SM::o_cnt, s_st = sb + SM::o_stats;
-    for (int c = lane; c < KT; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
+    const uint32_t s_key = sb + SM::o_key;
+    for (int c = lane; c < kSlots; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
+    if constexpr (HT > 0)
+        for (int c = lane; c < HT; c += kWarp) sm_st_u32(s_key + 4u * c, 0u);
     if (lane < 7) sm_st_u32(s_st + 4u * lane, 0u);
     __syncwarp();
     const uint2* __restrict__ pairs = p.pairs;
@@ -280,8 +295,11 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         }
         const float2 xb = __ldg(p.xb + i);
         const uint32_t own_col = p.col_ids ? (arg < p.k ? __ldg(p.col_of + arg) : kNone) : arg;
-        const uint32_t own_l = own_col - p.c0 < p.kt ? own_col - p.c0 : kNone;
-        if (lane == 0) sm_st_u32(s_cnt, 0u);
+        const uint32_t own_l = HT > 0 ? own_col : (own_col - p.c0 < p.kt ? own_col - p.c0 : kNone);
+        if (lane == 0) {
+            sm_st_u32(s_cnt, 0u);
+            if constexpr (HT > 0) sm_st_u32(s_cnt + 4u, 0u);  // hash table overflow of this document
+        }
         __syncwarp();
         double s_own = 0.0;
         int accmax = 0;      // ≥ every accumulator's final value (0: untouched clusters)
@@ -346,11 +364,41 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     if (pr.x != kNone && pr.x != own_l) {
                         const int qv = __float2int_rn(xq * __uint_as_float(pr.y));
                         if (qv != 0) {
-                            const int old = sm_atom_add(s_acc + 4u * pr.x, qv);
-                            accmax = max(accmax, old + qv);  // every final value is some old + qv
-                            if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
-                                const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
-                                if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr.x);
+                            if constexpr (HT > 0) {
+                                // linear probing from a multiplicative hash; the lane
+                                // that claims an empty slot records it as touched
+                                uint32_t h = (pr.x * 0x9E3779B1u) >> (32 - __builtin_ctz(HT));
+                                uint32_t slot = kNone;
+#pragma unroll 1
+                                for (int probe = 0; probe < 64; ++probe) {
+                                    uint32_t key = sm_ld_u32(s_key + 4u * h);
+                                    if (key == 0) {
+                                        key = sm_atom_cas(s_key + 4u * h, 0u, pr.x + 1u);
+                                        if (key == 0) {
+                                            const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
+                                            if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, h);
+                                            key = pr.x + 1u;
+                                        }
+                                    }
+                                    if (key == pr.x + 1u) {
+                                        slot = h;
+                                        break;
+                                    }
+                                    h = (h + 1u) & static_cast<uint32_t>(HT - 1);
+                                }
+                                if (slot != kNone) {
+                                    const int old = sm_atom_add(s_acc + 4u * slot, qv);
+                                    accmax = max(accmax, old + qv);
+                                } else {
+                                    sm_st_u32(s_cnt + 4u, 1u);  // table full: this document goes to the exact scan
+                                }
+                            } else {
+                                const int old = sm_atom_add(s_acc + 4u * pr.x, qv);
+                                accmax = max(accmax, old + qv);  // every final value is some old + qv
+                                if (old == 0) {  // first touch (a return to exactly 0 only duplicates)
+                                    const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
+                                    if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, pr.x);
+                                }
                             }
                         }
                     }
@@ -408,7 +456,13 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             // no cluster without a high entry shared with x can exceed lb
             // (the tile's low maxima bound the clusters of this tile only)
             const double lb = (p.single_tile ? lowb : theta_x1) + g64 * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
-            const bool take = best > lb && (INIT != kInitFull || arg < p.k);
+            bool take = best > lb && (INIT != kInitFull || arg < p.k);
+            if constexpr (HT > 0) {
+                if (sm_ld_u32(s_cnt + 4u) != 0) {
+                    take = false;
+                    stat(6, 1u);
+                }
+            }
             if (lane == 0) {
                 p.take[w] = take ? 1 : 0;
                 if (!take) {
@@ -418,7 +472,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             }
             active = take;
         }
-        const bool dense = ntouch > static_cast<uint32_t>(kCap);
+        const bool dense = ntouch > static_cast<uint32_t>(kCap);  // sweep every slot
         accmax = __reduce_max_sync(0xFFFFFFFFu, accmax);
         if (active) {
             // candidates: touched clusters whose upper bound reaches the running
@@ -427,7 +481,8 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             // and prunes the rest (a bound below best cannot win or tie)
             const double bx = lowb + (g32 + g64) * xb.y * p.cmax * (1.0 + 1e-12) + tiny;
             // no touched cluster can reach best: nothing to evaluate
-            const uint32_t count = static_cast<double>(accmax) * kFixUnit + bx >= best ? (dense ? p.kt : ntouch) : 0u;
+            const uint32_t count =
+                static_cast<double>(accmax) * kFixUnit + bx >= best ? (dense ? (HT > 0 ? kSlots : p.kt) : ntouch) : 0u;
             if (p.ub && lane == 0) {
                 // every other cluster j of this tile: s_j <= acc_j·2^-30 + bx <=
                 // accmax·2^-30 + bx (the own cluster's pairs were never
@@ -476,9 +531,18 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 double ub = 0.0;
                 if (kk < count) {
                     const uint32_t jl = dense ? kk : sm_ld_u16(s_tl + 2u * kk);
-                    gid = p.col_ids ? __ldg(p.col_ids + p.c0 + jl) : p.c0 + jl;
-                    ub = static_cast<double>(static_cast<int>(sm_ld_u32(s_acc + 4u * jl))) * kFixUnit + bx;
-                    cand = gid != arg && ub >= best;
+                    uint32_t col = p.c0 + jl;
+                    bool used = true;
+                    if constexpr (HT > 0) {
+                        const uint32_t key = sm_ld_u32(s_key + 4u * jl);
+                        used = key != 0;
+                        col = key - 1u;
+                    }
+                    if (used) {
+                        gid = p.col_ids ? __ldg(p.col_ids + col) : col;
+                        ub = static_cast<double>(static_cast<int>(sm_ld_u32(s_acc + 4u * jl))) * kFixUnit + bx;
+                        cand = gid != arg && ub >= best;
+                    }
                 }
                 unsigned cm = __ballot_sync(0xFFFFFFFFu, cand);
                 // place the new candidates into free lanes (evaluating pending
@@ -519,9 +583,15 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         // clear the touched accumulators
         __syncwarp();
         if (dense) {
-            for (int c = lane; c < KT; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
+            for (int c = lane; c < kSlots; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
+            if constexpr (HT > 0)
+                for (int c = lane; c < HT; c += kWarp) sm_st_u32(s_key + 4u * c, 0u);
         } else {
-            for (uint32_t kk = lane; kk < ntouch; kk += kWarp) sm_st_u32(s_acc + 4u * sm_ld_u16(s_tl + 2u * kk), 0u);
+            for (uint32_t kk = lane; kk < ntouch; kk += kWarp) {
+                const uint32_t sl = sm_ld_u16(s_tl + 2u * kk);
+                sm_st_u32(s_acc + 4u * sl, 0u);
+                if constexpr (HT > 0) sm_st_u32(s_key + 4u * sl, 0u);
+            }
         }
         __syncwarp();
     }
@@ -532,6 +602,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         atomicAdd(p.n_own, static_cast<unsigned long long>(sm_ld_u32(s_st + 12)));
         atomicAdd(p.n_cand, static_cast<unsigned long long>(sm_ld_u32(s_st + 16)));
         atomicAdd(p.n_cand_nnz, static_cast<unsigned long long>(sm_ld_u32(s_st + 20)));
+        if (HT > 0 && p.n_hovf) atomicAdd(p.n_hovf, static_cast<unsigned long long>(sm_ld_u32(s_st + 24)));
     }
 #undef w1
 }
@@ -631,15 +702,15 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
 // hptr[t] = (first pair, count, largest |value| below thr, 0). Pairs beyond
 // `cap` are not written (the host grows the buffer and rebuilds when
 // *total > cap).
-// With the nonzero bitmap nz of Cᵀ (M = Cᵀ; nullptr for other matrices), a
-// 16-byte group of a row is loaded only when one of its 4 columns is marked:
-// unmarked entries are zero, and most of a rare term's row is.
+// With `slack`, every list gets room to grow (cnt/4 + 2 slots, filled with
+// (kNone, 0)) and hptr[t].w = its capacity: the column rewrite then maintains
+// the lists in place from one iteration to the next (write_groups_kernel) —
+// removed entries become kNone holes, which the screen skips.
 __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
                                                            uint32_t c0, uint32_t kt, float thr,
                                                            uint4* __restrict__ hptr, uint2* __restrict__ pairs,
                                                            unsigned long long cap, unsigned long long* total,
-                                                           unsigned long long* overflow,
-                                                           const unsigned int* __restrict__ nz) {
+                                                           unsigned long long* overflow, int slack) {
     __shared__ uint32_t s_cnt[8];
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x / kWarp;
@@ -650,27 +721,9 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
         const float* row = M + t * ld + c0;
         uint32_t cnt = 0;
         float lowmax = 0.f, allmax = 0.f;
-        // the row's bitmap words of this tile: lane l holds words l and l + 32
-        unsigned ws0 = 0xFFFFFFFFu, ws1 = 0xFFFFFFFFu;
-        if (nz && t < d) {
-            const unsigned int* wrow = nz + t * (ld >> 5) + (c0 >> 5);
-            const uint32_t nw = (kt + 31) / 32;
-            ws0 = static_cast<uint32_t>(lane) < nw ? wrow[lane] : 0u;
-            ws1 = static_cast<uint32_t>(lane) + 32 < nw ? wrow[lane + 32] : 0u;
-        }
-        // marks of this lane's 4 columns 4·lane + 128·it .. + 3 (warp-uniform call)
-        auto bits4 = [&](uint32_t it) -> unsigned {
-            const uint32_t wsel = (static_cast<uint32_t>(lane) >> 3) + 4 * it;  // < 32 for every lane or none
-            const unsigned w = wsel < 32 ? __shfl_sync(0xFFFFFFFFu, ws0, wsel & 31)
-                                         : __shfl_sync(0xFFFFFFFFu, ws1, wsel & 31);
-            return (w >> (4 * (lane & 7))) & 0xFu;
-        };
         if (t < d) {
             // 16-byte loads over the row (tiles start at multiples of 4 columns)
-            for (uint32_t it = 0; it * 4u * kWarp < kt4; ++it) {
-                const uint32_t j = 4u * lane + it * 4u * kWarp;
-                const unsigned b4 = bits4(it);
-                if (j >= kt4 || b4 == 0) continue;
+            for (uint32_t j = 4u * lane; j < kt4; j += 4u * kWarp) {
                 const float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
                 const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -694,7 +747,8 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
             lowmax = fmaxf(lowmax, __shfl_xor_sync(0xFFFFFFFFu, lowmax, off));
             allmax = fmaxf(allmax, __shfl_xor_sync(0xFFFFFFFFu, allmax, off));
         }
-        if (lane == 0) s_cnt[warp] = cnt;
+        const uint32_t room = t < d ? cnt + (slack ? cnt / 4 + 2 : 0) : 0;
+        if (lane == 0) s_cnt[warp] = room;
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t sum = 0;
@@ -709,21 +763,22 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
             // a list past the buffer's end is dropped, and the term's bound then
             // covers every weight of the row (count 0, L_t = max |value|): the
             // screen stays exact, only looser (the host grows the buffer after)
-            const bool fits = b + cnt <= cap;
+            const bool fits = b + room <= cap;
             if (lane == 0) {
-                hptr[t] = fits ? make_uint4(static_cast<uint32_t>(b), cnt, __float_as_uint(lowmax), 0u)
+                hptr[t] = fits ? make_uint4(static_cast<uint32_t>(b), cnt, __float_as_uint(lowmax), room)
                                : make_uint4(0u, 0u, __float_as_uint(allmax), 0u);
                 if (!fits) atomicOr(overflow, 1ull);
             }
+            if (fits)
+                for (uint32_t q = cnt + lane; q < room; q += kWarp) pairs[b + q] = make_uint2(kNone, 0u);
             if (cnt > 0 && fits) {
                 // 16-byte loads again (the row is in L1/L2 now); each lane's kept
                 // values go to its prefix position within the 128 columns
                 uint32_t run = 0;
-                for (uint32_t it = 0; it * 4u * kWarp < kt4 && run < cnt; ++it) {
-                    const uint32_t j = 4u * lane + it * 4u * kWarp;
-                    const unsigned b4 = bits4(it);
+                for (uint32_t j0 = 0; j0 < kt4 && run < cnt; j0 += 4u * kWarp) {
+                    const uint32_t j = j0 + 4u * lane;
                     float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (j < kt4 && b4 != 0) v4 = __ldg(reinterpret_cast<const float4*>(row + j));
+                    if (j < kt4) v4 = __ldg(reinterpret_cast<const float4*>(row + j));
                     const float e[4] = {v4.x, v4.y, v4.z, v4.w};
                     uint32_t mine = 0;
 #pragma unroll
@@ -752,6 +807,23 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
         }
         __syncthreads();  // s_cnt / s_base reuse
     }
+}
+
+__global__ void doc_freq_kernel(const int32_t* __restrict__ idx, int64_t nnz, uint32_t* __restrict__ df) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(df + idx[e], 1u);
+}
+
+// Σ_t df_t · |high list of t| (the high pairs all documents would accumulate).
+__global__ void pairs_expect_kernel(const uint4* __restrict__ hptr, const uint32_t* __restrict__ df, uint32_t d,
+                                    unsigned long long* out) {
+    unsigned long long s = 0;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < d; t += gridDim.x * blockDim.x)
+        s += static_cast<unsigned long long>(df[t]) * hptr[t].y;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
 // NCC pass A over the bound-screened documents: queue the rescan exactly as

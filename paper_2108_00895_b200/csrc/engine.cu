@@ -51,6 +51,7 @@ struct Scalars {
     unsigned int n_unchanged;
     unsigned int bad;
     unsigned int zero_flag;
+    unsigned int hp_ovf;  // in-place high-postings maintenance ran out of room (rebuild)
     double objective;
 };
 
@@ -89,6 +90,7 @@ public:
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_HASH")) hash_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_DEBUG")) debug_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_THETA")) {
             theta_ = static_cast<float>(std::atof(e));
@@ -202,6 +204,7 @@ public:
         corpus_ = false;
         state_ = false;
         ub_valid_ = false;
+        df_ready_ = false;
         k_ = 0;
         if (n <= 0) throw InvalidArgument("empty corpus");
         if (dims == 0) throw InvalidArgument("dims must be positive");
@@ -301,6 +304,7 @@ public:
         if (!corpus_) throw InvalidArgument("upload a corpus before configuring");
         validate(c, static_cast<uint64_t>(n_total_));
         cfg_ = c;
+        hp_valid_ = false;
         lambdas_.assign(c.lambdas, c.lambdas + c.n_lambdas);
         cfg_.lambdas = lambdas_.data();
         // size every buffer for this (corpus, k); DevBuf::alloc only grows
@@ -328,6 +332,7 @@ public:
 
     // -------------------------------------------------------------- init --
     void reset_sums() {
+        hp_valid_ = false;  // Cᵀ is about to be (re)initialised
         CK(cudaMemsetAsync(S_.p, 0, static_cast<uint64_t>(d_) * ld_ * sizeof(long long), stream_));
         // every group marked: Cᵀ may hold values the fresh sums do not (seeds,
         // teacher forcing); the first rewrite clears the marks of empty groups
@@ -341,6 +346,7 @@ public:
 
     void init_from_seeds(const uint32_t* seeds_global) {
         need_config();
+        hp_valid_ = false;
         std::vector<uint32_t> local(k_);
         for (uint32_t j = 0; j < k_; ++j) {
             const int64_t g = seeds_global[j];
@@ -463,6 +469,7 @@ public:
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
         st->update_ms = ms;
+        last_update_ms_ = ms;
     }
 
     // Multi-GPU update: apply rows gathered from every rank, then finish.
@@ -966,6 +973,50 @@ public:
         CK(cudaStreamSynchronize(stream_));
     }
 
+    // Test hook: rebuilds the single-tile high postings of the current Cᵀ at the
+    // kept lists' θ and compares them row by row with the lists maintained in
+    // place (as sets of (column, value) pairs, holes ignored; the kept L_t must
+    // bound the fresh one). Returns the number of differing rows, or -1 when no
+    // maintained lists are held.
+    int64_t check_postings() {
+        need_state();
+        if (!hp_valid_) return -1;
+        const uint32_t kt = k_;
+        std::vector<uint4> h_old(d_), h_new(d_);
+        std::vector<uint2> p_old(pairs_.n);
+        CK(cudaMemcpyAsync(h_old.data(), hptr_.p, d_ * sizeof(uint4), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(p_old.data(), pairs_.p, pairs_.n * sizeof(uint2), cudaMemcpyDeviceToHost, stream_));
+        DevBuf<uint4> h2;
+        DevBuf<uint2> p2;
+        DevBuf<unsigned long long> c2;
+        h2.alloc(d_);
+        p2.alloc(pairs_.n * 2 + 1024);
+        c2.alloc(2);
+        CK(cudaMemsetAsync(c2.p, 0, 16, stream_));
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 32));
+        launch(hipost_build_kernel, grid, 256, static_cast<const float*>(ct_.p), (uint64_t)ld_, d_, 0u, kt, hp_theta_,
+               h2.p, p2.p, static_cast<unsigned long long>(p2.n), c2.p, c2.p + 1, 0);
+        CK_LAUNCH();
+        std::vector<uint2> p_new(p2.n);
+        CK(cudaMemcpyAsync(h_new.data(), h2.p, d_ * sizeof(uint4), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(p_new.data(), p2.p, p2.n * sizeof(uint2), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        int64_t bad = 0;
+        for (uint32_t t = 0; t < d_; ++t) {
+            std::vector<std::pair<uint32_t, uint32_t>> a, b;
+            for (uint32_t q = 0; q < h_old[t].y; ++q) {
+                const uint2 e = p_old[h_old[t].x + q];
+                if (e.x != kNone) a.emplace_back(e.x, e.y);
+            }
+            for (uint32_t q = 0; q < h_new[t].y; ++q) b.emplace_back(p_new[h_new[t].x + q].x, p_new[h_new[t].x + q].y);
+            std::sort(a.begin(), a.end());
+            std::sort(b.begin(), b.end());
+            const bool lbound = __builtin_bit_cast(float, h_old[t].z) >= __builtin_bit_cast(float, h_new[t].z);
+            if (a != b || !lbound) ++bad;
+        }
+        return bad;
+    }
+
     // Row / column slices of Cᵀ, gathered on the device in bounded chunks.
     void get_centroid_rows(uint32_t n_rows, const uint32_t* rows, float* out) {
         need_state();
@@ -1009,6 +1060,7 @@ public:
     // rebuilt from scratch by the next update.
     void set_centroids(const float* ct) {
         need_config();
+        hp_valid_ = false;
         if (!state_) set_state(nullptr, nullptr, iteration_);
         CK(cudaMemsetAsync(ct_.p, 0, static_cast<uint64_t>(d_) * ld_ * 4, stream_));
         CK(cudaMemcpy2DAsync(ct_.p, ld_ * sizeof(float), ct, k_ * sizeof(float), k_ * sizeof(float), d_,
@@ -1124,6 +1176,7 @@ public:
     // the seed documents gathered from whichever shard owns them.
     void init_from_rows(const int64_t* rptr, const int32_t* ridx, const float* rval) {
         need_config();
+        hp_valid_ = false;
         const int64_t nnz = rptr[k_];
         DevBuf<int64_t> dp;
         DevBuf<int32_t> di;
@@ -1367,7 +1420,8 @@ private:
         const uint32_t n_rb = static_cast<uint32_t>(ceil_div(d_, kRowBlock));
         const uint32_t n_groups = static_cast<uint32_t>(ceil_div(k_, 32));
         launch(write_groups_kernel, dim3(static_cast<unsigned>(ceil_div(n_groups, 4)), n_rb), 128, S_.p, ct_.p,
-               (uint64_t)ld_, d_, k_, touched_.p, Q_.p, part_.p, &scal_.p->zero_flag, nz_.p);
+               (uint64_t)ld_, d_, k_, touched_.p, Q_.p, part_.p, &scal_.p->zero_flag, nz_.p, hptr_.p, pairs_.p,
+               hp_valid_ ? hp_theta_ : 0.f, &scal_.p->hp_ovf);
         launch(reduce_groups_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 1024, part_.p, n_rb, k_, touched_.p,
                drift_.p, &scal_.p->n_rec);
         launch(flags_kernel, grid_for(k_, 256), 256, k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon,
@@ -1380,6 +1434,7 @@ private:
         pull_scalars();
         const uint32_t n_rec = hs_->n_rec;
         if (hs_->zero_flag) throw InvalidArgument("cannot normalize zero vector");
+        if (hs_->hp_ovf) hp_valid_ = false;
         n_unchanged_ = hs_->n_unchanged;
         // rewritten columns are fp32 roundings of unit vectors: ||c|| <= 1 + 2^-23
         if (n_rec > 0) cmax_ = (n_rec == k_) ? 1.0 + 0x1p-22 : std::max(cmax_, 1.0 + 0x1p-22);
@@ -1520,8 +1575,17 @@ private:
         btake_.alloc(n_);
         bctr_.alloc(8);
         CK(cudaMemsetAsync(bctr_.p, 0, 8 * sizeof(unsigned long long), stream_));
-        const float thr = theta_adapt_ ? tctl_[init].theta : theta_;
-        const uint32_t KT = ncols <= 1024 ? 1024 : 2048;
+        // more than one 2048-column tile: one pass with hash-table accumulators
+        // over every column (SSKM_HASH=0: a pass per tile)
+        const bool hash = ncols > 2048 && hash_enabled_;
+        const uint32_t KT = hash ? ncols : (ncols <= 1024 ? 1024 : 2048);
+        // single-pass lists over Cᵀ are kept from pass to pass, maintained in
+        // place by the column rewrite; rebuilt (and θ re-tuned) every
+        // kRebuildEvery assigns, or when they were invalidated
+        const bool lists_here = ncols <= KT && M == ct_.p;
+        const bool reuse = lists_here && hp_valid_ && assigns_since_build_ + 1 < kRebuildEvery &&
+                           (theta_adapt_ || theta_ == hp_theta_);
+        float thr = reuse ? hp_theta_ : (theta_adapt_ ? tctl_[init].theta : theta_);
         double pass_ms = 0.0, build_ms_inner = 0.0;
         BoundArgs p{};
         p.indptr = indptr_.p;
@@ -1556,6 +1620,7 @@ private:
         p.n_own = bctr_.p + 3;
         p.n_doc_nnz = bctr_.p + 4;
         p.n_cand_nnz = bctr_.p + 5;
+        p.n_hovf = bctr_.p + 6;
         // drift bound: single-tile full-scan passes over every document refresh
         // the per-document bounds; with valid bounds, a pre-pass first keeps
         // the documents that provably keep their cluster (skip_kernel)
@@ -1604,7 +1669,24 @@ private:
         for (uint32_t c0 = 0; c0 < ncols; c0 += KT) {
             const uint32_t kt = std::min<uint32_t>(KT, ncols - c0);
             if (c0 > 0) CK(cudaEventRecord(ev_[8], stream_));
-            build_hipost(M, ld, c0, kt, thr, ncols > KT);  // multi-tile: synchronises (capacity check)
+            if (reuse) {
+                ++assigns_since_build_;
+            } else {
+                build_hipost(M, ld, c0, kt, thr, ncols > KT || hash, lists_here);  // synchronises (capacity check)
+                // the hash tables hold a document's touched clusters: keep the
+                // expected high pairs per document (Σ_t df_t·|list_t| / N) near
+                // kHashPairs by raising θ before the screen (k = 50,000 needs a θ
+                // far above the tile screens')
+                for (int q = 0; hash && theta_adapt_ && q < 12; ++q) {
+                    const double per_doc = expected_pairs_per_doc();
+                    if (per_doc <= kHashPairs || thr >= 0.5f) break;
+                    thr = std::min(0.5f, thr * static_cast<float>(std::max(1.25, std::min(4.0, per_doc / kHashPairs))));
+                    tctl_[init].theta = thr;
+                    tctl_[init].last = -1.0;
+                    build_hipost(M, ld, c0, kt, thr, true, lists_here);
+                }
+                p.theta = static_cast<double>(thr);
+            }
             if (c0 > 0) {
                 CK(cudaEventRecord(ev_[9], stream_));
                 CK(cudaEventSynchronize(ev_[9]));
@@ -1624,7 +1706,9 @@ private:
             // brackets every tile's screen, and the postings builds between
             // tiles are timed separately (build_ms) and subtracted
             if (c0 == 0) CK(cudaEventRecord(ev_[6], stream_));
-            if (KT == 1024)
+            if (hash)
+                bound_launch_hash(p, init);
+            else if (KT == 1024)
                 bound_launch<1024>(p, init);
             else
                 bound_launch<2048>(p, init);
@@ -1636,7 +1720,7 @@ private:
                    sims_start_.p, sims_.p, unchanged_.p, rescan_.p, &scal_.p->n_rescan);
         // θ for the next assign: keep the exact-scan share small and the
         // candidate dots near one per document (θ never changes a result)
-        unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0}, hp[2] = {0, 0}, sk[4] = {0, 0, 0, 0};
+        unsigned long long ctr[7] = {0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0}, sk[4] = {0, 0, 0, 0};
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hp, hpctr_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
@@ -1652,7 +1736,8 @@ private:
         }
         scalars_fresh_ = true;
         if (hp[0] > pairs_.n) grow_pairs(hp[0]);  // the last tile's lists overflowed: room for the next pass
-        last_hp_overflow_ = hp[1] != 0;
+        if (!reuse) last_hp_overflow_ = hp[1] != 0;
+        if (last_hp_overflow_) hp_valid_ = false;
         const uint64_t n_fb = hs_->n_exact;
         {
             float ms = 0.f;
@@ -1682,21 +1767,70 @@ private:
         // per work item (θ trades high pairs against candidate dots, and the
         // balance differs per corpus); back off when documents fall through to
         // the exact scan. θ never changes a result.
+        // θ is tuned per period between list rebuilds (it can only change at a
+        // rebuild): the cost of a period is its screen and update time per
+        // document; hill-climb it (×1.25 / ×0.8, reversing when it rises), and
+        // back off when documents fall through to the exact scan
         if (theta_adapt_ && n_work > 0) {
             ThetaCtl& c = tctl_[init];
-            const double fb = static_cast<double>(n_fb) / static_cast<double>(n_work);
-            const double cost = pass_ms / static_cast<double>(n_work);
-            if (fb > 2e-3) {
-                c.theta *= 0.7f;
-                c.dir = -1;
-                c.last = -1.0;
-            } else {
-                if (c.last > 0.0 && cost > c.last * 1.02) c.dir = -c.dir;
-                c.last = cost;
-                c.theta *= c.dir > 0 ? 1.25f : 0.8f;
+            c.acc_ms += pass_ms + (init == kInitFull ? last_update_ms_ : 0.0);
+            c.acc_n += static_cast<double>(n_);
+            c.acc_fb += static_cast<double>(n_fb - std::min<uint64_t>(n_fb, ctr[6]));
+            c.acc_hovf += static_cast<double>(ctr[6]);
+            c.acc_work += static_cast<double>(n_work);
+            const bool period_end = !lists_here || assigns_since_build_ + 1 >= kRebuildEvery || !hp_valid_;
+            if (period_end) {
+                const double fb = c.acc_fb / c.acc_work;
+                const double cost = c.acc_ms / c.acc_n;
+                if (c.acc_hovf > 1e-4 * c.acc_work) {  // hash tables overflow: fewer high pairs
+                    c.theta *= 1.3f;
+                    c.dir = 1;
+                    c.last = -1.0;
+                } else if (fb > 2e-3) {
+                    c.theta *= 0.7f;
+                    c.dir = -1;
+                    c.last = -1.0;
+                } else {
+                    if (c.last > 0.0 && cost > c.last * 1.02) c.dir = -c.dir;
+                    c.last = cost;
+                    c.theta *= c.dir > 0 ? 1.25f : 0.8f;
+                }
+                c.theta = std::min(0.25f, std::max(1e-5f, c.theta));
+                c.acc_ms = c.acc_n = c.acc_fb = c.acc_work = c.acc_hovf = 0.0;
             }
-            c.theta = std::min(0.25f, std::max(1e-5f, c.theta));
         }
+    }
+
+    static constexpr int kHashSlots = 1024;  // per-warp hash accumulators (4 KB keys + 4 KB sums)
+    static constexpr double kHashPairs = 192.0;  // target high pairs per document in hash passes
+
+    // Σ_t df_t · (high-list length of t) / N for the lists just built: the high
+    // pairs an average document accumulates. df_ (document frequencies) once.
+    double expected_pairs_per_doc() {
+        if (!df_ready_) {
+            df_.alloc(d_);
+            CK(cudaMemsetAsync(df_.p, 0, d_ * sizeof(uint32_t), stream_));
+            launch(doc_freq_kernel, grid_for(nnz_, 256), 256, idx_.p, nnz_, df_.p);
+            CK_LAUNCH();
+            df_ready_ = true;
+        }
+        CK(cudaMemsetAsync(&scal_.p->n_moved, 0, 8, stream_));
+        launch(pairs_expect_kernel, grid_for(d_, 256), 256, hptr_.p, df_.p, d_, &scal_.p->n_moved);
+        CK_LAUNCH();
+        unsigned long long tot = 0;
+        CK(cudaMemcpyAsync(&tot, &scal_.p->n_moved, 8, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        return static_cast<double>(tot) / static_cast<double>(std::max<int64_t>(1, n_));
+    }
+
+    void bound_launch_hash(const BoundArgs& p, int init) {
+        using SM = BoundSmem<2048, kHashSlots>;
+        if (init == kInitFull)
+            bound_launch_k(bound_screen_kernel<2048, kInitFull, kHashSlots>, SM::per_warp, p);
+        else if (init == kInitNcc)
+            bound_launch_k(bound_screen_kernel<2048, kInitNcc, kHashSlots>, SM::per_warp, p);
+        else
+            bound_launch_k(bound_screen_kernel<2048, kInitRescan, kHashSlots>, SM::per_warp, p);
     }
 
     template <int KT>
@@ -1757,18 +1891,26 @@ private:
     // passes, whose first tile bounds the later tiles' clusters by θ·‖x‖₁);
     // without, an overflow only loosens the bound (the dropped lists' weights
     // are covered by L_t) and the host grows the buffer after the pass.
-    void build_hipost(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr, bool check) {
+    // `slack`: the single-tile lists over Cᵀ, built with room to be maintained
+    // in place by the column rewrite until the next rebuild.
+    void build_hipost(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr, bool check,
+                      bool slack = false) {
         hptr_.alloc(d_);
         hpctr_.alloc(2);
+        hp_valid_ = false;
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 32));
         for (int attempt = 0; attempt < 2; ++attempt) {
             CK(cudaMemsetAsync(hpctr_.p, 0, 2 * sizeof(unsigned long long), stream_));
             // the screen addresses pairs with 32-bit offsets: lists past 2^32 are
             // dropped (exact, looser bound) rather than truncated
             launch(hipost_build_kernel, grid, 256, M, ld, d_, c0, kt, thr, hptr_.p, pairs_.p,
-                   std::min<unsigned long long>(pairs_.n, 0xFFFFFFFFull), hpctr_.p, hpctr_.p + 1,
-                   M == ct_.p ? static_cast<const unsigned int*>(nz_.p) : nullptr);
+                   std::min<unsigned long long>(pairs_.n, 0xFFFFFFFFull), hpctr_.p, hpctr_.p + 1, slack ? 1 : 0);
             CK_LAUNCH();
+            if (slack) {
+                hp_valid_ = true;  // withdrawn after the pass if a list was dropped
+                hp_theta_ = thr;
+                assigns_since_build_ = 0;
+            }
             if (!check) return;
             unsigned long long total = 0;
             CK(cudaMemcpyAsync(&total, hpctr_.p, 8, cudaMemcpyDeviceToHost, stream_));
@@ -1780,6 +1922,7 @@ private:
 
     void grow_pairs(unsigned long long total) {
         if (total >= (1ull << 32)) throw std::runtime_error("bound screen: high postings exceed 2^32 pairs");
+        hp_valid_ = false;
         pairs_.alloc(static_cast<size_t>(total) * 3 / 2 + 1);
     }
 
@@ -1823,6 +1966,7 @@ private:
     // Postings of the columns [c0, c0 + kt) of M into pptr_ / pairs_: per-term
     // counts, exclusive scan, bank-interleaved fill. Returns the pair count.
     uint32_t build_postings(const float* M, uint64_t ld, uint32_t c0, uint32_t kt, float thr = 0.f) {
+        hp_valid_ = false;  // the pair buffer is shared with the high postings
         pcnt_.alloc(d_ + 1);
         pptr_.alloc(d_ + 1);
         CK(cudaMemsetAsync(pcnt_.p + d_, 0, 4, stream_));
@@ -2172,7 +2316,8 @@ private:
     struct ThetaCtl {
         float theta = 0.004f;  // adaptive split, per pass kind (full, NCC pass A, rescan)
         int dir = 1;
-        double last = -1.0;    // screen ms per work item at the previous step
+        double last = -1.0;    // cost per document of the previous period
+        double acc_ms = 0.0, acc_n = 0.0, acc_fb = 0.0, acc_work = 0.0, acc_hovf = 0.0;  // the current period
     };
     ThetaCtl tctl_[3];
     // per-assign bound-screen totals (stats)
@@ -2188,7 +2333,16 @@ private:
     DevBuf<unsigned long long> skip_ctr_;
     std::vector<double> dcum_h_;
     bool ub_valid_ = false;     // every document's bound is valid for the current assignments
+    // high postings kept across passes (single cluster tile over Cᵀ)
+    static constexpr uint32_t kRebuildEvery = 4;
+    bool hp_valid_ = false;     // hptr_/pairs_ hold exactly Cᵀ's entries >= hp_theta_
+    float hp_theta_ = 0.f;
+    uint32_t assigns_since_build_ = 0;
+    double last_update_ms_ = 0.0;  // the last update's device time (θ tuning)
     bool skip_enabled_ = true;  // SSKM_SKIP=0: screen every document
+    bool hash_enabled_ = true;  // SSKM_HASH=0: multi-tile passes instead of one hash-accumulator pass
+    DevBuf<uint32_t> df_;       // document frequency per term (hash-pass θ)
+    bool df_ready_ = false;
     uint64_t skip_docs_ = 0;
     double skip_ms_ = 0.0;  // dots the kernels evaluated in the current assign (gpu_dot_products)
     bool nonneg_ = true;
@@ -2444,6 +2598,10 @@ int sskm_get_centroid_rows(sskm_ctx* ctx, uint32_t n_rows, const uint32_t* rows,
 
 int sskm_get_centroid_cols(sskm_ctx* ctx, uint32_t n_cols, const uint32_t* cols, float* out) {
     return guard([&] { E(ctx).get_centroid_cols(n_cols, cols, out); });
+}
+
+int sskm_debug_check_postings(sskm_ctx* ctx, int64_t* bad_rows) {
+    return guard([&] { *bad_rows = E(ctx).check_postings(); });
 }
 
 int sskm_set_centroids(sskm_ctx* ctx, const float* ct) {

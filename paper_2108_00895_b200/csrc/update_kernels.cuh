@@ -292,12 +292,58 @@ constexpr int kRowBlock = 512;  // rows per partial in the column reductions
 // words are empty, so most of S and Cᵀ is never read. Per (row block, column)
 // the drift partial is an ascending-row fp64 sum (unmarked rows would add
 // exact zeros); the partials are reduced in a fixed association below.
+// In-place maintenance of the bound screen's high postings (hipost_build_kernel
+// with slack) for one rewritten row t of the warp's column group g: an entry
+// that was high and still is gets its new value, one that stopped being high
+// becomes a kNone hole, one that became high is appended (a full list raises
+// *ovf: the host rebuilds), and a new low value raises L_t. The lists then hold
+// exactly the entries >= thr of the new Cᵀ, as a rebuild would (up to order and
+// holes, which the screen's integer accumulation does not see), and L_t stays an
+// upper bound on the row's low weights.
+__device__ __forceinline__ void hipost_maintain(uint4* __restrict__ hptr, uint2* __restrict__ pairs, uint32_t t,
+                                                uint32_t g, uint32_t j, bool chg, float old, float cn, float thr,
+                                                unsigned int* ovf, int lane) {
+    const bool oh = chg && old != 0.f && fabsf(old) >= thr;
+    const bool nh = chg && cn != 0.f && fabsf(cn) >= thr;
+    const bool lo = chg && !nh && cn != 0.f;
+    const unsigned m_oh = __ballot_sync(0xFFFFFFFFu, oh);
+    if (!__any_sync(0xFFFFFFFFu, oh || nh || lo)) return;
+    const uint4 h = hptr[t];
+    if (lo && fabsf(cn) > __uint_as_float(h.z)) atomicMax(&hptr[t].z, __float_as_uint(fabsf(cn)));
+    int slot = -1;  // this lane's entry in the row's list (old-high entries)
+    for (uint32_t s0 = 0; m_oh && s0 < h.y; s0 += kWarp) {
+        const uint32_t sl = s0 + lane;
+        const uint32_t c = sl < h.y ? pairs[h.x + sl].x : kNone;
+        unsigned mm = __ballot_sync(0xFFFFFFFFu, c != kNone && (c >> 5) == g);
+        while (mm) {
+            const int src = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const uint32_t col = __shfl_sync(0xFFFFFFFFu, c, src);
+            if (static_cast<uint32_t>(lane) == (col & 31u)) slot = static_cast<int>(s0) + src;
+        }
+    }
+    if (oh) {
+        if (slot >= 0)
+            pairs[h.x + slot] = nh ? make_uint2(j, __float_as_uint(cn)) : make_uint2(kNone, 0u);
+        else
+            atomicOr(ovf, 1u);  // not in the list: the lists no longer describe Cᵀ
+    } else if (nh) {
+        const uint32_t pos = atomicAdd(&hptr[t].y, 1u);
+        if (pos < h.w)
+            pairs[h.x + pos] = make_uint2(j, __float_as_uint(cn));
+        else
+            atomicOr(ovf, 1u);
+    }
+}
+
 __global__ void __launch_bounds__(128) write_groups_kernel(const long long* __restrict__ S, float* __restrict__ CT,
                                                            uint64_t ld, uint32_t d, uint32_t k,
                                                            const uint8_t* __restrict__ touched,
                                                            const unsigned long long* __restrict__ Q,
                                                            double* __restrict__ part, unsigned int* zero_flag,
-                                                           unsigned int* __restrict__ nz) {
+                                                           unsigned int* __restrict__ nz, uint4* __restrict__ hptr,
+                                                           uint2* __restrict__ pairs, float hthr,
+                                                           unsigned int* hp_ovf) {
     const int lane = threadIdx.x & (kWarp - 1);
     const uint32_t g = blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
     const uint32_t rb = blockIdx.y;
@@ -341,15 +387,24 @@ __global__ void __launch_bounds__(128) write_groups_kernel(const long long* __re
                 sv[q] = on[q] ? __ldcs(S + o) : 0;
                 old[q] = on[q] ? CT[o] : 0.f;
             }
+            float cn[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
+                cn[q] = (!on[q] || sv[q] == 0) ? 0.f : static_cast<float>(static_cast<double>(sv[q]) * inv);
                 if (!on[q]) continue;
                 const uint64_t o = static_cast<uint64_t>(tb + r[q]) * ld + j;
-                const float cn = sv[q] == 0 ? 0.f : static_cast<float>(static_cast<double>(sv[q]) * inv);
-                const double diff = static_cast<double>(cn) - static_cast<double>(old[q]);
+                const double diff = static_cast<double>(cn[q]) - static_cast<double>(old[q]);
                 dr = fma(diff, diff, dr);
-                if (cn != old[q]) CT[o] = cn;
+                if (cn[q] != old[q]) CT[o] = cn[q];
                 if (sv[q] == 0) atomicAnd(nz + static_cast<uint64_t>(tb + r[q]) * wpr + g, ~lbit);
+            }
+            if (hthr > 0.f) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (r[q] < 0) break;
+                    hipost_maintain(hptr, pairs, tb + r[q], g, j, on[q] && cn[q] != old[q], old[q], cn[q], hthr,
+                                    hp_ovf, lane);
+                }
             }
         }
     }

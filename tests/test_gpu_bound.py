@@ -52,6 +52,7 @@ CASES = {
     "one_tile": lambda: (S.generate(3000, 4096, 24, 60.0, seed=11), 64),
     "two_tiles": lambda: (S.generate(6000, 8192, 300, 50.0, seed=12), 2100),
     "signed": lambda: (signed_corpus(2500, 800, 5), 40),
+    "five_tiles": lambda: (S.generate(12000, 8192, 600, 40.0, seed=13), 9000),
 }
 
 
@@ -69,6 +70,11 @@ def test_theta_and_screen_invariance(case, mode, monkeypatch):
         # the fixed split was the one used (passes that ran the bound screen)
         assert any(x > 0 for x in th) and all(x == 0 or x == pytest.approx(float(theta), rel=1e-6) for x in th)
     monkeypatch.delenv("SSKM_THETA")
+    if k > 2048:  # one hash-accumulator pass by default; a pass per 2048-cluster tile without
+        monkeypatch.setenv("SSKM_HASH", "0")
+        t, _ = trajectory(m, k, seeds, mode, iters)
+        assert_same(ref, t, "tile passes")
+        monkeypatch.delenv("SSKM_HASH")
     monkeypatch.setenv("SSKM_BOUND", "0")
     t, th = trajectory(m, k, seeds, mode, iters)
     assert_same(ref, t, "postings screen")
@@ -114,7 +120,7 @@ def test_postings_overflow_stays_exact(case, monkeypatch):
     assert_same(ref, t, "pairs cap 64")
 
 
-@pytest.mark.parametrize("case", ["one_tile", "two_tiles", "signed"])
+@pytest.mark.parametrize("case", ["one_tile", "two_tiles", "signed", "five_tiles"])
 def test_drift_bound_skip_is_exact(case, monkeypatch):
     """Documents kept in their cluster by the drift bound (skip_test_kernel)
     must leave exactly the trajectory of screening every document
@@ -144,3 +150,25 @@ def test_drift_bound_skip_is_exact(case, monkeypatch):
     assert s0 == 0
     assert s1 > 0
     assert_same(ref, got, f"skip {case}")
+
+
+@pytest.mark.parametrize("case", ["one_tile", "signed", "two_tiles"])
+def test_kept_postings_equal_a_rebuild(case):
+    """The high postings kept across iterations and maintained in place by the
+    column rewrite (hipost_maintain) hold exactly the entries a fresh build at
+    the same θ would, after every update and assign."""
+    m, k = CASES[case]()
+    eng = P.Engine(0)
+    eng.upload(m)
+    eng.configure(k, mode="baseline", conv_sq_dist=1e-300, max_iters=20)
+    eng.init_from_seeds(S.init_seeds(m.n_docs, k, 0))
+    checked = 0
+    for _ in range(14):
+        eng.update()
+        bad = eng.debug_check_postings()
+        assert bad in (-1, 0), bad
+        checked += bad == 0
+        eng.assign()
+        bad = eng.debug_check_postings()
+        assert bad in (-1, 0), bad
+    assert checked >= 5  # the lists were kept (not rebuilt) on most updates
