@@ -42,6 +42,7 @@ struct RunConfig {
     std::uint64_t seed = 0;
     std::uint32_t threads = 0;   // accepted for API parity; the GPU grid replaces it
     int device = 0;              // CUDA device ordinal
+    std::vector<int> devices;    // several GPUs of this node (documents sharded; needs init_seeds)
     std::vector<std::uint32_t> init_seeds;  // empty: k-means++ (engine.cpp:66-130)
 
     sskm_run_config c() const {
@@ -126,11 +127,21 @@ inline ClusteringResult run(const CsrCorpus& data, const RunConfig& cfg, bool wi
     out.iterations.resize(cfg.max_iters);
     std::uint32_t n_it = 0;
     std::int32_t stop = 0;
-    check(sskm_cluster_csr(&r, static_cast<std::int64_t>(data.size()), data.dims, data.indptr.data(),
-                           data.indices.data(), data.values.data(),
-                           cfg.init_seeds.empty() ? nullptr : cfg.init_seeds.data(), out.assignments.data(),
-                           out.sims.data(), with_centroids ? out.centroids_t.data() : nullptr, out.iterations.data(),
-                           cfg.max_iters, &n_it, &stop, &out.objective));
+    if (!cfg.devices.empty()) {  // multi-device context (sskm_multi_*): bitwise the single-GPU result
+        if (cfg.init_seeds.empty()) throw std::invalid_argument("a multi-device run needs init_seeds");
+        check(sskm_cluster_csr_multi(&r, static_cast<std::int32_t>(cfg.devices.size()), cfg.devices.data(),
+                                     static_cast<std::int64_t>(data.size()), data.dims, data.indptr.data(),
+                                     data.indices.data(), data.values.data(), cfg.init_seeds.data(),
+                                     out.assignments.data(), out.sims.data(),
+                                     with_centroids ? out.centroids_t.data() : nullptr, out.iterations.data(),
+                                     cfg.max_iters, &n_it, &stop, &out.objective));
+    } else {
+        check(sskm_cluster_csr(&r, static_cast<std::int64_t>(data.size()), data.dims, data.indptr.data(),
+                               data.indices.data(), data.values.data(),
+                               cfg.init_seeds.empty() ? nullptr : cfg.init_seeds.data(), out.assignments.data(),
+                               out.sims.data(), with_centroids ? out.centroids_t.data() : nullptr,
+                               out.iterations.data(), cfg.max_iters, &n_it, &stop, &out.objective));
+    }
     out.iterations.resize(n_it);
     out.stop_reason = static_cast<StopReason>(stop);
     return out;

@@ -159,7 +159,9 @@ def load():
     if override:
         lib = C.CDLL(override)
         for name, res, args in SIGNATURES:
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)  # an older build (A/B runs) may lack newer entry points
+            if fn is None:
+                continue
             fn.restype = res
             fn.argtypes = args
         _lib = lib

@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
 // hptr[t] = (first pair, count, largest |value| below thr, 0). Pairs beyond
 // `cap` are not written (the host grows the buffer and rebuilds when
 // *total > cap).
-// With `slack`, every list gets room to grow (cnt/4 + 2 slots, filled with
+// With `slack`, every list gets room to grow (cnt/2 + 4 slots, filled with
 // (kNone, 0)) and hptr[t].w = its capacity: the column rewrite then maintains
 // the lists in place from one iteration to the next (write_groups_kernel) —
 // removed entries become kNone holes, which the screen skips.
@@ -747,7 +747,7 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
             lowmax = fmaxf(lowmax, __shfl_xor_sync(0xFFFFFFFFu, lowmax, off));
             allmax = fmaxf(allmax, __shfl_xor_sync(0xFFFFFFFFu, allmax, off));
         }
-        const uint32_t room = t < d ? cnt + (slack ? cnt / 4 + 2 : 0) : 0;
+        const uint32_t room = t < d ? cnt + (slack ? cnt / 2 + 4 : 0) : 0;
         if (lane == 0) s_cnt[warp] = room;
         __syncthreads();
         if (threadIdx.x == 0) {

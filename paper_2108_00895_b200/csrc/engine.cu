@@ -90,14 +90,17 @@ public:
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_KEEP_LISTS")) keep_lists_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_HASH")) hash_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_DEBUG")) debug_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_THETA")) {
             theta_ = static_cast<float>(std::atof(e));
             theta_adapt_ = false;
         }
-        if (const char* e = std::getenv("SSKM_THETA0"))  // starting point of the adaptive θ
-            for (auto& c : tctl_) c.theta = static_cast<float>(std::atof(e));
+        if (const char* e = std::getenv("SSKM_THETA0")) {  // starting point of the adaptive θ
+            theta0_ = static_cast<float>(std::atof(e));
+            theta0_set_ = true;
+        }
         if (const char* e = std::getenv("SSKM_POST_KT")) post_kt_max_ = static_cast<uint32_t>(std::atoi(e));
         if (const char* e = std::getenv("SSKM_POST_WARPS")) post_warps_ = std::max(1, std::min(8, std::atoi(e)));
         if (const char* e = std::getenv("SSKM_DENSE_ABOVE")) dense_above_ = std::atof(e);
@@ -305,6 +308,19 @@ public:
         validate(c, static_cast<uint64_t>(n_total_));
         cfg_ = c;
         hp_valid_ = false;
+        // θ per pass kind: tile passes start from the mean document length
+        // (measured optima: 0.004 for 41 terms, 0.003 for 69,
+        // 0.0005 for 650 — long documents make candidate dots dear, so a
+        // lower θ, more high pairs and tighter bounds pay); hash passes from 0.02
+        {
+            const double len = static_cast<double>(nnz_) / static_cast<double>(std::max<int64_t>(1, n_));
+            const float t0 = theta0_set_ ? theta0_
+                                         : static_cast<float>(std::min(0.01, std::max(2e-4, 0.003 * std::pow(69.0 / std::max(1.0, len), 0.8))));
+            for (auto& q : tctl_) q = ThetaCtl{};
+            for (auto& q : tctl_) q.theta = t0;
+            hash_theta0_ = theta0_set_ ? theta0_ : 0.02f;
+            hash_theta_started_ = false;
+        }
         lambdas_.assign(c.lambdas, c.lambdas + c.n_lambdas);
         cfg_.lambdas = lambdas_.data();
         // size every buffer for this (corpus, k); DevBuf::alloc only grows
@@ -1421,7 +1437,7 @@ private:
         const uint32_t n_groups = static_cast<uint32_t>(ceil_div(k_, 32));
         launch(write_groups_kernel, dim3(static_cast<unsigned>(ceil_div(n_groups, 4)), n_rb), 128, S_.p, ct_.p,
                (uint64_t)ld_, d_, k_, touched_.p, Q_.p, part_.p, &scal_.p->zero_flag, nz_.p, hptr_.p, pairs_.p,
-               hp_valid_ ? hp_theta_ : 0.f, &scal_.p->hp_ovf);
+               keep_lists_ && hp_valid_ ? hp_theta_ : 0.f, &scal_.p->hp_ovf);
         launch(reduce_groups_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 1024, part_.p, n_rb, k_, touched_.p,
                drift_.p, &scal_.p->n_rec);
         launch(flags_kernel, grid_for(k_, 256), 256, k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon,
@@ -1583,8 +1599,12 @@ private:
         // place by the column rewrite; rebuilt (and θ re-tuned) every
         // kRebuildEvery assigns, or when they were invalidated
         const bool lists_here = ncols <= KT && M == ct_.p;
-        const bool reuse = lists_here && hp_valid_ && assigns_since_build_ + 1 < kRebuildEvery &&
+        const bool reuse = keep_lists_ && lists_here && hp_valid_ && assigns_since_build_ + 1 < kRebuildEvery &&
                            (theta_adapt_ || theta_ == hp_theta_);
+        if (hash && theta_adapt_ && !hash_theta_started_) {  // the first hash pass of this configuration
+            for (auto& q : tctl_) q.theta = std::max(q.theta, hash_theta0_);
+            hash_theta_started_ = true;
+        }
         float thr = reuse ? hp_theta_ : (theta_adapt_ ? tctl_[init].theta : theta_);
         double pass_ms = 0.0, build_ms_inner = 0.0;
         BoundArgs p{};
@@ -1673,18 +1693,19 @@ private:
                 ++assigns_since_build_;
             } else {
                 build_hipost(M, ld, c0, kt, thr, ncols > KT || hash, lists_here);  // synchronises (capacity check)
-                // the hash tables hold a document's touched clusters: keep the
-                // expected high pairs per document (Σ_t df_t·|list_t| / N) near
-                // kHashPairs by raising θ before the screen (k = 50,000 needs a θ
+                // hash passes: the tables hold a document's touched clusters, so
+                // θ is raised until the expected high pairs per document,
+                // Σ_t df_t·|list_t| / N for the lists just built, is within the
+                // target (pairs ∝ θ^-1/2 on these corpora; k = 50,000 needs a θ
                 // far above the tile screens')
-                for (int q = 0; hash && theta_adapt_ && q < 12; ++q) {
+                for (int q = 0; hash && theta_adapt_ && q < 8; ++q) {
                     const double per_doc = expected_pairs_per_doc();
-                    if (per_doc <= kHashPairs || thr >= 0.5f) break;
-                    thr = std::min(0.5f, thr * static_cast<float>(std::max(1.25, std::min(4.0, per_doc / kHashPairs))));
-                    tctl_[init].theta = thr;
-                    tctl_[init].last = -1.0;
+                    const double tgt = tctl_[init].target;
+                    if (per_doc <= tgt * 1.4 || thr >= 0.5f) break;
+                    thr = std::min(0.5f, static_cast<float>(thr * std::min(2.0, per_doc / tgt)));
                     build_hipost(M, ld, c0, kt, thr, true, lists_here);
                 }
+                tctl_[init].theta = thr;
                 p.theta = static_cast<double>(thr);
             }
             if (c0 > 0) {
@@ -1767,42 +1788,35 @@ private:
         // per work item (θ trades high pairs against candidate dots, and the
         // balance differs per corpus); back off when documents fall through to
         // the exact scan. θ never changes a result.
-        // θ is tuned per period between list rebuilds (it can only change at a
-        // rebuild): the cost of a period is its screen and update time per
-        // document; hill-climb it (×1.25 / ×0.8, reversing when it rises), and
-        // back off when documents fall through to the exact scan
+        // θ follows the failures, per period of kRebuildEvery passes (θ only
+        // changes at a rebuild): lower (tighter low-part bounds) when documents
+        // fall through to the exact scan; in hash passes, a lower pairs target
+        // when tables overflow. Otherwise θ stays: on these corpora the step
+        // time is flat over a wide θ range once the lists are kept (measured,
+        // DESIGN.md §3.1), and comparing costs across converging iterations
+        // misleads a hill climb.
         if (theta_adapt_ && n_work > 0) {
             ThetaCtl& c = tctl_[init];
-            c.acc_ms += pass_ms + (init == kInitFull ? last_update_ms_ : 0.0);
-            c.acc_n += static_cast<double>(n_);
             c.acc_fb += static_cast<double>(n_fb - std::min<uint64_t>(n_fb, ctr[6]));
             c.acc_hovf += static_cast<double>(ctr[6]);
             c.acc_work += static_cast<double>(n_work);
-            const bool period_end = !lists_here || assigns_since_build_ + 1 >= kRebuildEvery || !hp_valid_;
-            if (period_end) {
-                const double fb = c.acc_fb / c.acc_work;
-                const double cost = c.acc_ms / c.acc_n;
-                if (c.acc_hovf > 1e-4 * c.acc_work) {  // hash tables overflow: fewer high pairs
+            if (!lists_here || ++c.passes >= kRebuildEvery) {
+                if (c.acc_hovf > 1e-4 * c.acc_work) {
+                    c.target *= 0.7;
                     c.theta *= 1.3f;
-                    c.dir = 1;
-                    c.last = -1.0;
-                } else if (fb > 2e-3) {
+                } else if (c.acc_fb > 2e-3 * c.acc_work) {
+                    c.target *= 1.4;
                     c.theta *= 0.7f;
-                    c.dir = -1;
-                    c.last = -1.0;
-                } else {
-                    if (c.last > 0.0 && cost > c.last * 1.02) c.dir = -c.dir;
-                    c.last = cost;
-                    c.theta *= c.dir > 0 ? 1.25f : 0.8f;
                 }
-                c.theta = std::min(0.25f, std::max(1e-5f, c.theta));
-                c.acc_ms = c.acc_n = c.acc_fb = c.acc_work = c.acc_hovf = 0.0;
+                c.target = std::min(1024.0, std::max(8.0, c.target));
+                c.theta = std::min(0.5f, std::max(1e-5f, c.theta));
+                c.acc_fb = c.acc_work = c.acc_hovf = 0.0;
+                c.passes = 0;
             }
         }
     }
 
     static constexpr int kHashSlots = 1024;  // per-warp hash accumulators (4 KB keys + 4 KB sums)
-    static constexpr double kHashPairs = 192.0;  // target high pairs per document in hash passes
 
     // Σ_t df_t · (high-list length of t) / N for the lists just built: the high
     // pairs an average document accumulates. df_ (document frequencies) once.
@@ -1863,10 +1877,14 @@ private:
     template <typename K>
     std::pair<int, int> pick_bound_cfg(K k, size_t per_warp) {
         int warps = 1, per_sm = 1, best = 0;
+        // the attribute is per device and function, and engines of a
+        // multi-device context (several may share a device) pick their
+        // configurations concurrently: it is only ever raised to one common
+        // ceiling, never lowered under another engine's launch
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(200u << 10)));
         for (int w : {8, 4, 2}) {
             const size_t sm = static_cast<size_t>(w) * per_warp;
             if (sm > (200u << 10)) continue;
-            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
             int b = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, w * 32, sm));
             if (b * w > best) {
@@ -1876,7 +1894,6 @@ private:
             }
         }
         const size_t smem = static_cast<size_t>(warps) * per_warp;
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         if (debug_)
             std::fprintf(stderr, "[sskm] bound launch: %d warps/block, %d blocks/SM, %zu B smem/block\n", warps, per_sm,
                          smem);
@@ -2314,10 +2331,10 @@ private:
     bool debug_ = false;  // SSKM_DEBUG=1: per-assign screen counters on stderr
     float theta_ = 0.004f;        // fixed high/low split of the centroid weights (SSKM_THETA)
     struct ThetaCtl {
-        float theta = 0.004f;  // adaptive split, per pass kind (full, NCC pass A, rescan)
-        int dir = 1;
-        double last = -1.0;    // cost per document of the previous period
-        double acc_ms = 0.0, acc_n = 0.0, acc_fb = 0.0, acc_work = 0.0, acc_hovf = 0.0;  // the current period
+        float theta = 0.004f;   // adaptive split, per pass kind (full, NCC pass A, rescan)
+        double target = 192.0;  // hash passes: high pairs per document
+        double acc_fb = 0.0, acc_work = 0.0, acc_hovf = 0.0;  // the current period
+        uint32_t passes = 0;
     };
     ThetaCtl tctl_[3];
     // per-assign bound-screen totals (stats)
@@ -2336,6 +2353,9 @@ private:
     // high postings kept across passes (single cluster tile over Cᵀ)
     static constexpr uint32_t kRebuildEvery = 4;
     bool hp_valid_ = false;     // hptr_/pairs_ hold exactly Cᵀ's entries >= hp_theta_
+    bool keep_lists_ = true;    // SSKM_KEEP_LISTS=0: rebuild the high postings every assign
+    float theta0_ = 0.004f, hash_theta0_ = 0.02f;
+    bool theta0_set_ = false, hash_theta_started_ = false;
     float hp_theta_ = 0.f;
     uint32_t assigns_since_build_ = 0;
     double last_update_ms_ = 0.0;  // the last update's device time (θ tuning)

@@ -1,5 +1,5 @@
 // C++ drop-in example: the reference's sskm::run call shape on the B200 core.
-// Usage: run_example validate | run <k>
+// Usage: run_example validate | run <k> | multi <k>
 #include <cstdio>
 #include <cstring>
 #include <random>
@@ -45,6 +45,7 @@ int main(int argc, char** argv) {
     cfg.k = argc > 2 ? static_cast<std::uint32_t>(std::atoi(argv[2])) : 4;
     cfg.mode = sskm_b200::parse_mode("ncc");
     cfg.init_seeds = {0, 1, 2, 3};
+    if (!std::strcmp(what, "multi")) cfg.devices = {0, 0};  // two document shards (on one device here)
     try {
         auto r = sskm_b200::run(data, cfg);
         std::printf("iterations=%zu stop=%s objective=%.12f dots=%llu a0=%u a1=%u a2=%u a3=%u\n", r.iterations.size(),

@@ -39,3 +39,12 @@ def test_cpp_run_matches_python_api(exe):
     assert r.returncode == 0, r.stdout + r.stderr
     assert "stop=no_reassignments" in r.stdout
     assert "a0=0 a1=1 a2=2 a3=3" in r.stdout  # 4 orthogonal groups, seeds 0..3 one per group
+
+
+@pytest.mark.gpu
+def test_cpp_multi_device_run_equals_single(exe):
+    """RunConfig::devices (sskm_cluster_csr_multi): the same result line."""
+    one = subprocess.run([exe, "run", "4"], capture_output=True, text=True)
+    two = subprocess.run([exe, "multi", "4"], capture_output=True, text=True)
+    assert two.returncode == 0, two.stdout + two.stderr
+    assert two.stdout == one.stdout
