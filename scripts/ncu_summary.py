@@ -1,9 +1,11 @@
 """Summarise one kernel of an ncu --set full report into profiles/<out>.json
-(used by bench.py's roofline.traffic). usage: ncu_summary.py REPORT OUT.json [SOURCE-NOTE]"""
+(used by bench.py's roofline.traffic).
+usage: ncu_summary.py REPORT OUT.json [SOURCE-NOTE [ALGORITHMIC-BYTES-OF-THE-LAUNCH]]"""
 import csv, io, json, subprocess, sys
 
 rep, out = sys.argv[1], sys.argv[2]
 note = sys.argv[3] if len(sys.argv) > 3 else ""
+alg = float(sys.argv[4]) if len(sys.argv) > 4 else None  # algorithmic bytes of the captured launch
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units, v = rows[0], rows[1], rows[2]
@@ -52,6 +54,11 @@ for k in list(m):
         val = num(k)
         if val:
             s["stall_" + k[len("smsp__pcsamp_warps_issue_stalled_"):]] = val
+if alg:
+    s["algorithmic_bytes_per_launch"] = alg
+    s["traffic_over_algorithmic"] = dram / alg if alg else None
+    s["achieved_algorithmic_GBs"] = alg / (s["gpu_time_ms"] / 1e3) / 1e9 if s["gpu_time_ms"] else None
+s["capture"] = note
 with open(out, "w") as f:
     json.dump(s, f, indent=1)
 print(json.dumps(s, indent=1))

@@ -34,7 +34,11 @@ for it in range(1, iters + 1):
                           "screen": st.screen_ms, "theta": st.bound_theta, "moved": st.n_moved, "own": st.bound_own_dots,
                           "reassigned": st.n_reassigned, "recomputed": st.n_recomputed, "exact": st.n_exact,
                           "skip_docs": st.skip_docs, "skip_ms": st.skip_ms,
-                          "launches": st.screen_launches, "wall": time.perf_counter() - t0}), flush=True)
+                          "launches": st.screen_launches, "wall": time.perf_counter() - t0,
+                          "pairs": st.bound_pairs, "doc_nnz": st.bound_doc_nnz, "visits": st.bound_visits,
+                          "cand": st.bound_candidates, "cand_nnz": st.bound_cand_nnz,
+                          "alg_bytes": 8 * st.bound_pairs + 16 * st.bound_doc_nnz + 36 * st.bound_visits
+                                       + 4 * st.bound_cand_nnz}), flush=True)
         continue
     ct = eng.get_centroids()
     d = np.sqrt(((ct.astype(np.float64) - prev) ** 2).sum(0))
