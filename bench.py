@@ -114,8 +114,8 @@ class ClockSampler:
 
 def ncu_traffic():
     """Per-launch DRAM bytes of the bound screen from the committed ncu capture of
-    this bench command (profiles/ncu_bound_summary.json)."""
-    p = os.path.join(ROOT, "profiles", "ncu_bound_summary.json")
+    this bench command (profiles/r02_ncu_bound_summary.json)."""
+    p = os.path.join(ROOT, "profiles", "r02_ncu_bound_summary.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
@@ -243,7 +243,7 @@ def bound_roofline(stats, data):
            "note": "algorithmic bytes of the bound screen = 8·high pairs + 16·doc nnz read + 36·doc visits "
                    "+ 4·candidate-dot nnz (DESIGN.md §3.1), over the kernel's CUDA-event time; "
                    "traffic = ncu dram__bytes_read+write per launch of the same bench command "
-                   "(profiles/ncu_bound_summary.json)"}
+                   "(profiles/r02_ncu_bound_summary.json)"}
     if traffic and summ:
         out["traffic_over_algorithmic"] = traffic / summ.get("algorithmic_bytes_per_launch", bb["bytes"])
         out["traffic_capture"] = summ.get("capture", "")

@@ -703,9 +703,10 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
 // `cap` are not written (the host grows the buffer and rebuilds when
 // *total > cap).
 // With `slack`, every list gets room to grow (cnt/2 + 4 slots, filled with
-// (kNone, 0)) and hptr[t].w = its capacity: the column rewrite then maintains
-// the lists in place from one iteration to the next (write_groups_kernel) —
-// removed entries become kNone holes, which the screen skips.
+// (kNone, 0)) and hptr[t].w = (sorted length << 16) | capacity: the column
+// rewrite then maintains the lists in place from one iteration to the next
+// (hipost_maintain); a row without room (w = 0) raises the rebuild flag on its
+// first append.
 __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
                                                            uint32_t c0, uint32_t kt, float thr,
                                                            uint4* __restrict__ hptr, uint2* __restrict__ pairs,
@@ -747,7 +748,10 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
             lowmax = fmaxf(lowmax, __shfl_xor_sync(0xFFFFFFFFu, lowmax, off));
             allmax = fmaxf(allmax, __shfl_xor_sync(0xFFFFFFFFu, allmax, off));
         }
-        const uint32_t room = t < d ? cnt + (slack ? cnt / 2 + 4 : 0) : 0;
+        // with slack: room for cnt/2 + 4 more (capacity and sorted length share
+        // hptr.w as 16-bit halves, so rows past 40,000 entries get none)
+        const bool grow = slack && cnt <= 40000u;
+        const uint32_t room = t < d ? cnt + (grow ? cnt / 2 + 4 : 0) : 0;
         if (lane == 0) s_cnt[warp] = room;
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -765,7 +769,8 @@ __global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restri
             // screen stays exact, only looser (the host grows the buffer after)
             const bool fits = b + room <= cap;
             if (lane == 0) {
-                hptr[t] = fits ? make_uint4(static_cast<uint32_t>(b), cnt, __float_as_uint(lowmax), room)
+                hptr[t] = fits ? make_uint4(static_cast<uint32_t>(b), cnt, __float_as_uint(lowmax),
+                                            grow ? (cnt << 16) | room : 0u)
                                : make_uint4(0u, 0u, __float_as_uint(allmax), 0u);
                 if (!fits) atomicOr(overflow, 1ull);
             }

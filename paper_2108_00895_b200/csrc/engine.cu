@@ -385,8 +385,11 @@ public:
         CK(cudaStreamSynchronize(stream_));
     }
 
-    // Single-GPU k-means++ (engine.cpp:66-130). The per-round cumulative sum
-    // runs on the host in document order so the picks are the reference's.
+    // Single-GPU k-means++ (engine.cpp:66-130), device-resident: per round the
+    // seed's dots (kpp_round_kernel), the weights and their double-double prefix,
+    // and an exact pick from bracketed sequential sums (kpp_pick_kernel); 16
+    // bytes come back per round. A round whose pick the brackets cannot decide
+    // (or SSKM_KPP_HOST=1) is replayed on the host in document order, as before.
     void init_kmeanspp(uint64_t seed, uint32_t* seeds_out) {
         need_config();
         if (n_ != n_total_) throw InvalidArgument("k-means++ seeding needs the whole corpus on one GPU");
@@ -397,43 +400,59 @@ public:
             return i < n ? i : n - 1;
         };
         const size_t n = static_cast<size_t>(n_);
+        const bool host_only = std::getenv("SSKM_KPP_HOST") && std::atoi(std::getenv("SSKM_KPP_HOST")) != 0;
         std::vector<uint8_t> chosen(n, 0);
-        std::vector<double> sims(n), cum(n);
-        std::vector<int64_t> ptr(n + 1);
-        CK(cudaMemcpyAsync(ptr.data(), indptr_.p, (n + 1) * 8, cudaMemcpyDeviceToHost, stream_));
+        std::vector<double> sims, cum;
         DevBuf<float> dense;
         dense.alloc(d_);
+        DevBuf<uint8_t> dchosen;
+        dchosen.alloc(n);
+        DevBuf<double2> w, E;
+        w.alloc(n);
+        E.alloc(n);
+        DevBuf<unsigned long long> ab;
+        ab.alloc(2);
+        size_t scan_bytes = 0;
+        CK(cub::DeviceScan::InclusiveScan(nullptr, scan_bytes, w.p, E.p, KppDD{}, static_cast<int>(n), stream_));
+        DevBuf<unsigned char> scan_tmp;
+        scan_tmp.alloc(scan_bytes);
         CK(cudaMemsetAsync(dense.p, 0, d_ * sizeof(float), stream_));
+        CK(cudaMemsetAsync(dchosen.p, 0, n, stream_));
         launch(fill_u32_kernel, grid_for(n_, 256), 256, a_.p, n_, 0);
         launch(fill_f64_kernel, grid_for(n_, 256), 256, sims_.p, n_, -2.0);
         CK_LAUNCH();
         std::vector<uint32_t> seeds;
+        kpp_host_rounds_ = 0;
         auto add_seed = [&](size_t doc, uint32_t cluster) {
             chosen[doc] = 1;
             seeds.push_back(static_cast<uint32_t>(doc));
+            launch(set_u8_kernel, 1, 1, dchosen.p, static_cast<int64_t>(doc), static_cast<uint8_t>(1));
             launch(scatter_row_kernel, 1, 256, indptr_.p, idx_.p, val_.p, doc, dense.p, 0);
-            launch(kpp_round_kernel, grid_for(n_ * 32, 256), 256, indptr_.p, idx_.p, val_.p, n_,
-                                                                          dense.p, cluster, a_.p, sims_.p);
+            launch(kpp_round_kernel, grid_for(n_, 256), 256, indptr_.p, idx_.p, val_.p, n_, dense.p, cluster, a_.p,
+                   sims_.p);
             launch(scatter_row_kernel, 1, 256, indptr_.p, idx_.p, val_.p, doc, dense.p, 1);
             CK_LAUNCH();
         };
-        add_seed(uniform_index(n), 0);
-        for (uint32_t c = 1; c < k_; ++c) {
+        // the reference's sequential round (engine.cpp:101-126) on the host
+        auto host_round = [&](bool have_u, double u) -> size_t {
+            sims.resize(n);
+            cum.resize(n);
             CK(cudaMemcpyAsync(sims.data(), sims_.p, n * 8, cudaMemcpyDeviceToHost, stream_));
             CK(cudaStreamSynchronize(stream_));
+            ++kpp_host_rounds_;
             double total = 0.0;
             for (size_t i = 0; i < n; ++i) {
-                double w = 0.0;
+                double wv = 0.0;
                 if (!chosen[i]) {
                     const double dd = 1.0 - sims[i];
-                    if (dd > 0.0) w = dd * dd;
+                    if (dd > 0.0) wv = dd * dd;
                 }
-                total += w;
+                total += wv;
                 cum[i] = total;
             }
             size_t pick;
             if (total > 0.0) {
-                const double target = uniform_unit() * total;
+                const double target = (have_u ? u : uniform_unit()) * total;
                 pick = static_cast<size_t>(std::upper_bound(cum.begin(), cum.end(), target) - cum.begin());
                 if (pick >= n) {
                     pick = n - 1;
@@ -443,9 +462,47 @@ public:
                 pick = 0;
                 while (chosen[pick]) ++pick;
             }
+            return pick;
+        };
+        add_seed(uniform_index(n), 0);
+        bool pending = false;  // a draw taken from the generator, not yet consumed by a round
+        double u = 0.0;
+        for (uint32_t c = 1; c < k_; ++c) {
+            size_t pick;
+            if (host_only) {
+                pick = host_round(false, 0.0);
+            } else {
+                launch(kpp_weights_kernel, grid_for(n_, 256), 256, sims_.p, dchosen.p, n_, w.p);
+                size_t tb = scan_bytes;
+                CK(cub::DeviceScan::InclusiveScan(scan_tmp.p, tb, w.p, E.p, KppDD{}, static_cast<int>(n), stream_));
+                ++launches_;
+                // the draw of this round (the reference consumes it only when the total is positive)
+                if (!pending) {
+                    u = uniform_unit();
+                    pending = true;
+                }
+                const unsigned long long init[2] = {static_cast<unsigned long long>(n), static_cast<unsigned long long>(n)};
+                CK(cudaMemcpyAsync(ab.p, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
+                launch(kpp_pick_kernel, grid_for(n_, 256), 256, E.p, n_, u, ab.p);
+                CK_LAUNCH();
+                unsigned long long res[2];
+                double2 last;
+                CK(cudaMemcpyAsync(res, ab.p, sizeof(res), cudaMemcpyDeviceToHost, stream_));
+                CK(cudaMemcpyAsync(&last, E.p + (n - 1), sizeof(last), cudaMemcpyDeviceToHost, stream_));
+                CK(cudaStreamSynchronize(stream_));
+                const bool positive = last.x + last.y > 0.0;  // a sum of nonnegative terms is 0 only if all are
+                if (positive && res[0] == res[1] && res[0] < n) {
+                    pick = static_cast<size_t>(res[0]);
+                    pending = false;
+                } else if (positive) {
+                    pick = host_round(true, u);
+                    pending = false;
+                } else {
+                    pick = host_round(true, u);  // total = 0: the lowest unchosen document; the draw stays pending
+                }
+            }
             add_seed(pick, c);
-        }
-        // Cᵀ = the seed documents (informational; the first update recomputes all)
+        }        // Cᵀ = the seed documents (informational; the first update recomputes all)
         DevBuf<uint32_t> dseeds;
         dseeds.alloc(k_);
         CK(cudaMemcpyAsync(dseeds.p, seeds.data(), k_ * 4, cudaMemcpyHostToDevice, stream_));
@@ -989,10 +1046,10 @@ public:
         CK(cudaStreamSynchronize(stream_));
     }
 
-    // Test hook: rebuilds the single-tile high postings of the current Cᵀ at the
+    // Test hook: rebuilds the single-pass high postings of the current Cᵀ at the
     // kept lists' θ and compares them row by row with the lists maintained in
-    // place (as sets of (column, value) pairs, holes ignored; the kept L_t must
-    // bound the fresh one). Returns the number of differing rows, or -1 when no
+    // place (as sets of (column, value) pairs, zero pairs ignored; the kept L_t
+    // must bound the fresh one). Returns the number of differing rows, or -1 when no
     // maintained lists are held.
     int64_t check_postings() {
         need_state();
@@ -1022,7 +1079,7 @@ public:
             std::vector<std::pair<uint32_t, uint32_t>> a, b;
             for (uint32_t q = 0; q < h_old[t].y; ++q) {
                 const uint2 e = p_old[h_old[t].x + q];
-                if (e.x != kNone) a.emplace_back(e.x, e.y);
+                if (e.x != kNone && e.y != 0u) a.emplace_back(e.x, e.y);  // zero pairs: entries no longer high
             }
             for (uint32_t q = 0; q < h_new[t].y; ++q) b.emplace_back(p_new[h_new[t].x + q].x, p_new[h_new[t].x + q].y);
             std::sort(a.begin(), a.end());
@@ -2359,6 +2416,7 @@ private:
     float hp_theta_ = 0.f;
     uint32_t assigns_since_build_ = 0;
     double last_update_ms_ = 0.0;  // the last update's device time (θ tuning)
+    uint64_t kpp_host_rounds_ = 0;  // k-means++ rounds the host had to replay (last seeding)
     bool skip_enabled_ = true;  // SSKM_SKIP=0: screen every document
     bool hash_enabled_ = true;  // SSKM_HASH=0: multi-tile passes instead of one hash-accumulator pass
     DevBuf<uint32_t> df_;       // document frequency per term (hash-pass θ)

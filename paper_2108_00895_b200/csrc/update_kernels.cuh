@@ -293,46 +293,52 @@ constexpr int kRowBlock = 512;  // rows per partial in the column reductions
 // the drift partial is an ascending-row fp64 sum (unmarked rows would add
 // exact zeros); the partials are reduced in a fixed association below.
 // In-place maintenance of the bound screen's high postings (hipost_build_kernel
-// with slack) for one rewritten row t of the warp's column group g: an entry
-// that was high and still is gets its new value, one that stopped being high
-// becomes a kNone hole, one that became high is appended (a full list raises
-// *ovf: the host rebuilds), and a new low value raises L_t. The lists then hold
-// exactly the entries >= thr of the new Cᵀ, as a rebuild would (up to order and
-// holes, which the screen's integer accumulation does not see), and L_t stays an
-// upper bound on the row's low weights.
+// with slack) for one rewritten row t of the warp's column group g. A row's
+// list is its columns in ascending order (as built; hptr.w = (sorted length <<
+// 16) | capacity) followed by columns appended since. An entry that changed and
+// is high, or was, is looked up by its own lane (binary search in the sorted
+// part, then the short tail): it gets its new value — or 0 when it is no longer
+// high (the screen adds nothing for a zero pair, and the column keeps its place,
+// so the order survives); a newly high entry not in the list is appended (a full
+// list raises *ovf: the host rebuilds); a new low value raises L_t. The lists
+// then hold exactly the entries >= thr of the new Cᵀ (plus zero pairs), and L_t
+// stays an upper bound on the row's low weights.
 __device__ __forceinline__ void hipost_maintain(uint4* __restrict__ hptr, uint2* __restrict__ pairs, uint32_t t,
-                                                uint32_t g, uint32_t j, bool chg, float old, float cn, float thr,
-                                                unsigned int* ovf, int lane) {
+                                                uint32_t j, bool chg, float old, float cn, float thr,
+                                                unsigned int* ovf) {
     const bool oh = chg && old != 0.f && fabsf(old) >= thr;
     const bool nh = chg && cn != 0.f && fabsf(cn) >= thr;
     const bool lo = chg && !nh && cn != 0.f;
-    const unsigned m_oh = __ballot_sync(0xFFFFFFFFu, oh);
     if (!__any_sync(0xFFFFFFFFu, oh || nh || lo)) return;
     const uint4 h = hptr[t];
     if (lo && fabsf(cn) > __uint_as_float(h.z)) atomicMax(&hptr[t].z, __float_as_uint(fabsf(cn)));
-    int slot = -1;  // this lane's entry in the row's list (old-high entries)
-    for (uint32_t s0 = 0; m_oh && s0 < h.y; s0 += kWarp) {
-        const uint32_t sl = s0 + lane;
-        const uint32_t c = sl < h.y ? pairs[h.x + sl].x : kNone;
-        unsigned mm = __ballot_sync(0xFFFFFFFFu, c != kNone && (c >> 5) == g);
-        while (mm) {
-            const int src = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const uint32_t col = __shfl_sync(0xFFFFFFFFu, c, src);
-            if (static_cast<uint32_t>(lane) == (col & 31u)) slot = static_cast<int>(s0) + src;
-        }
+    if (!(oh || nh)) return;
+    const uint32_t sorted = h.w >> 16, cap = h.w & 0xFFFFu;
+    const uint2* __restrict__ row = pairs + h.x;
+    // binary search in the sorted part
+    uint32_t a = 0, b = sorted;
+    while (a < b) {
+        const uint32_t m = (a + b) >> 1;
+        if (row[m].x < j) a = m + 1; else b = m;
     }
-    if (oh) {
-        if (slot >= 0)
-            pairs[h.x + slot] = nh ? make_uint2(j, __float_as_uint(cn)) : make_uint2(kNone, 0u);
-        else
-            atomicOr(ovf, 1u);  // not in the list: the lists no longer describe Cᵀ
+    int slot = (a < sorted && row[a].x == j) ? static_cast<int>(a) : -1;
+    if (slot < 0)  // appended since the last build
+        for (uint32_t q = sorted; q < min(h.y, cap); ++q)
+            if (row[q].x == j) {
+                slot = static_cast<int>(q);
+                break;
+            }
+    const uint2 e = make_uint2(j, nh ? __float_as_uint(cn) : 0u);
+    if (slot >= 0) {
+        pairs[h.x + slot] = e;
     } else if (nh) {
         const uint32_t pos = atomicAdd(&hptr[t].y, 1u);
-        if (pos < h.w)
-            pairs[h.x + pos] = make_uint2(j, __float_as_uint(cn));
+        if (pos < cap)
+            pairs[h.x + pos] = e;
         else
             atomicOr(ovf, 1u);
+    } else {
+        atomicOr(ovf, 1u);  // an entry that was high is not in the list: the lists no longer describe Cᵀ
     }
 }
 
@@ -402,8 +408,7 @@ __global__ void __launch_bounds__(128) write_groups_kernel(const long long* __re
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (r[q] < 0) break;
-                    hipost_maintain(hptr, pairs, tb + r[q], g, j, on[q] && cn[q] != old[q], old[q], cn[q], hthr,
-                                    hp_ovf, lane);
+                    hipost_maintain(hptr, pairs, tb + r[q], j, on[q] && cn[q] != old[q], old[q], cn[q], hthr, hp_ovf);
                 }
             }
         }
@@ -583,32 +588,90 @@ __global__ void kpp_round_kernel(const int64_t* __restrict__ indptr, const int32
                                  const float* __restrict__ val, int64_t n,
                                  const float* __restrict__ dense_seed, uint32_t cluster,
                                  uint32_t* __restrict__ a, double* __restrict__ sims) {
-    const int lane = threadIdx.x & (kWarp - 1);
-    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * blockDim.x / kWarp;
-    for (uint64_t i = gw; i < static_cast<uint64_t>(n); i += nw) {
+    // a thread per document, its entries in ascending order (the reference's
+    // summation order); four gathers in flight per thread
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t beg = indptr[i], end = indptr[i + 1];
         double s = 0.0;
-        for (int64_t e0 = beg; e0 < end; e0 += kWarp) {
-            const int64_t e = e0 + lane;
-            float x_l = 0.f, c_l = 0.f;
-            if (e < end) {
-                x_l = val[e];
-                c_l = dense_seed[idx[e]];
+        int64_t e = beg;
+        for (; e + 4 <= end; e += 4) {
+            int32_t t[4];
+            float x[4], c[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                t[r] = __ldg(idx + e + r);
+                x[r] = __ldg(val + e + r);
             }
-            const int cnt = static_cast<int>(imin64(kWarp, end - e0));
-            for (int j = 0; j < cnt; ++j) {
-                const double x = static_cast<double>(__shfl_sync(0xFFFFFFFFu, x_l, j));
-                const double c = static_cast<double>(__shfl_sync(0xFFFFFFFFu, c_l, j));
-                s = fma(x, c, s);
-            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) c[r] = __ldg(dense_seed + t[r]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s = fma(static_cast<double>(x[r]), static_cast<double>(c[r]), s);
         }
-        if (lane == 0 && s > sims[i]) {
+        for (; e < end; ++e) s = fma(static_cast<double>(__ldg(val + e)), static_cast<double>(__ldg(dense_seed + __ldg(idx + e))), s);
+        if (s > sims[i]) {
             sims[i] = s;
             a[i] = cluster;
         }
     }
 }
+
+// ---------------------------------------------------------- k-means++ --
+// Device-resident k-means++ rounds (engine.cpp:99-128). The reference draws
+// target = u · total and picks the first document whose running fp64 sum
+// cum[i] (sequential, document order) exceeds it. The weights w_i are computed
+// exactly as the reference does; their prefix is scanned in double-double
+// (error ≤ n·2^-104 relative), and the sequential sums are bracketed:
+// |cum[i] − E_i| ≤ γ(i+1)·E_i for nonnegative terms, so are the total and the
+// target. The first index that may exceed the target (a) and the first that
+// certainly does (b) are found by atomicMin over all documents; a == b decides
+// the pick exactly. Otherwise (a near-tie with the target, the rare `pick ≥ n`
+// and `total = 0` branches) the host replays the round sequentially.
+struct KppDD {
+    __device__ __forceinline__ double2 operator()(const double2& a, const double2& b) const {
+        const double s = a.x + b.x;
+        const double v = s - a.x;
+        double e = (a.x - (s - v)) + (b.x - v);
+        e += a.y + b.y;
+        const double hi = s + e;
+        return make_double2(hi, e - (hi - s));
+    }
+};
+
+__global__ void kpp_weights_kernel(const double* __restrict__ sims, const uint8_t* __restrict__ chosen, int64_t n,
+                                   double2* __restrict__ w) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double x = 0.0;
+        if (!chosen[i]) {
+            const double d = 1.0 - sims[i];
+            if (d > 0.0) x = d * d;
+        }
+        w[i] = make_double2(x, 0.0);
+    }
+}
+
+// out[0] = a, out[1] = b (initialised to n by the host)
+__global__ void kpp_pick_kernel(const double2* __restrict__ E, int64_t n, double u, unsigned long long* out) {
+    const double2 en = E[n - 1];
+    const double tot = en.x + en.y;
+    const double dd = static_cast<double>(n) * 0x1p-104 * tot;  // the double-double scan's own error
+    const double gn = static_cast<double>(n) * 0x1p-53;
+    const double err_n = gn * (1.0 + 2.0 * gn) * tot + dd;
+    const double t_lo = u * (tot - err_n) * (1.0 - 0x1p-50);
+    const double t_hi = u * (tot + err_n) * (1.0 + 0x1p-50);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double2 e = E[i];
+        const double ei = e.x + e.y;
+        const double g = static_cast<double>(i + 1) * 0x1p-53;
+        const double err = (g * (1.0 + 2.0 * g) * ei + dd) * (1.0 + 0x1p-50) + 0x1p-1000;
+        if (ei + err > t_lo) atomicMin(out + 0, static_cast<unsigned long long>(i));
+        if (ei - err > t_hi) atomicMin(out + 1, static_cast<unsigned long long>(i));
+    }
+}
+
+__global__ void set_u8_kernel(uint8_t* p, int64_t i, uint8_t v) { p[i] = v; }
 
 __global__ void scatter_row_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
                                    const float* __restrict__ val, int64_t row, float* __restrict__ dense,

@@ -346,3 +346,27 @@ def test_gpu_cluster_cached_engine_reshapes():
         out.append(r.objective)
     assert out[0] == out[2]
     _lib.check(_lib.load().sskm_release_cache())
+
+
+@pytest.mark.parametrize("k", [100, 400])
+def test_gpu_kmeanspp_device_rounds_match_reference(k, monkeypatch):
+    """Device-resident k-means++ rounds (bracketed sequential sums, exact pick)
+    give the reference's seeds, the host-replayed rounds' seeds, and the same
+    nearest-seed state, on config 0."""
+    m = S.corpus(S.CONFIGS["c0"])
+    eng = engine_for(m, k)
+    seeds = eng.init_kmeanspp(5)
+    a, s, _ = eng.get_state()
+    monkeypatch.setenv("SSKM_KPP_HOST", "1")
+    eng2 = engine_for(m, k)
+    seeds2 = eng2.init_kmeanspp(5)
+    a2, s2, _ = eng2.get_state()
+    np.testing.assert_array_equal(seeds, seeds2)
+    np.testing.assert_array_equal(a, a2)
+    np.testing.assert_array_equal(s, s2)
+    if O.ref_available():
+        c = O.Corpus(m.indptr, m.indices, m.values.astype(np.float64), m.dims)
+        rs, ra, rsims = O.seed_kmeanspp(c, k, 5)
+        np.testing.assert_array_equal(seeds, rs)
+        np.testing.assert_array_equal(a, ra)
+        np.testing.assert_array_equal(s, rsims)
