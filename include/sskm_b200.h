@@ -254,6 +254,35 @@ int sskm_update_apply(sskm_ctx* ctx, int64_t n_moved, const uint32_t* old_c, con
 /* Local partials for the assign step's scalars (sums over the shard). */
 int sskm_local_sims_sum(sskm_ctx* ctx, double* sum);
 
+/* GPU TF-IDF ingestion: vectorize_corpus (corpus.hpp:60-88, corpus.cpp:101-134;
+ * Python binding bindings.cpp:53-63), bit-identical to the reference.
+ * Documents are one byte array `text` with n_docs + 1 nondecreasing offsets
+ * (the caller keeps the ids); stop words likewise (n_stop strings). Errors as
+ * the reference: SSKM_ERUNTIME "empty corpus" / "empty vocabulary",
+ * SSKM_EINVAL "max_df_ratio must be in (0, 1]". The result handle holds host
+ * copies: the CSR rows (fp64 values, int32 dims ascending), the input document
+ * index of each row, the dropped documents in the reference's order (stop-word
+ * documents first, then rows that vectorised to zero), doc_freq by dim,
+ * Vocabulary::n_docs and the vocabulary strings in dim order. */
+typedef struct sskm_vec sskm_vec;
+int sskm_vectorize(int32_t device, int64_t n_docs, const char* text, const int64_t* text_offsets, int64_t n_stop,
+                   const char* stop_text, const int64_t* stop_offsets, double max_df_ratio, sskm_vec** out);
+int sskm_vec_sizes(const sskm_vec* v, int64_t* n_rows, int64_t* nnz, uint32_t* dims, uint32_t* n_docs_vocab,
+                   int64_t* n_dropped, int64_t* vocab_bytes);
+/* Any output pointer may be NULL (skipped). vocab_offsets has dims + 1 entries. */
+int sskm_vec_export(const sskm_vec* v, int64_t* indptr, int32_t* indices, double* values, int64_t* kept_docs,
+                    int64_t* dropped_docs, uint32_t* doc_freq, char* vocab_text, int64_t* vocab_offsets);
+/* Device time of the pipeline (upload to the last kernel), kernels launched,
+ * tokens, rows that needed Brent's cycle search in normalize. */
+int sskm_vec_stats(const sskm_vec* v, double* gpu_ms, uint64_t* launches, uint64_t* n_tokens, uint64_t* brent_rows);
+int sskm_vec_free(sskm_vec* v);
+/* normalize (sparse_vector.hpp:60-63, sparse_vector.cpp:158-209) of every row
+ * of a host CSR on the GPU, bit-identical to the reference (iterated unit step,
+ * period-2 rule, Brent's cycle search). Outputs sized like the inputs; rows can
+ * only lose entries whose quotient underflows. */
+int sskm_normalize_csr(int32_t device, int64_t n_rows, const int64_t* indptr, const int32_t* indices,
+                       const double* values, int64_t* out_indptr, int32_t* out_indices, double* out_values);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,6 +132,13 @@ def _load(kind: str):
         lib.sref_seed_kmeanspp.argtypes = [_P, C.c_uint32, C.c_uint64, C.c_uint32, _u32p, _u32p, _f64p]
         lib.sref_validate.argtypes = [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
                                       _f64p, C.c_uint32]
+        lib.sref_vectorize.argtypes = [C.c_int64, C.c_char_p, _i64p, C.c_int64, C.c_char_p, _i64p, C.c_double,
+                                       C.POINTER(_P)]
+        lib.sref_vec_sizes.argtypes = [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_uint32), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_double)]
+        lib.sref_vec_export.argtypes = [_P, _i64p, _u32p, _f64p, _i64p, _i64p, _u32p, C.c_char_p, _i64p]
+        lib.sref_vec_free.argtypes = [_P]
         lib.sref_load_matrix.restype = _P
         lib.sref_load_matrix.argtypes = [C.c_char_p]
         lib.sref_write_matrix.argtypes = [C.c_char_p, _P]
@@ -556,3 +563,49 @@ def ref_report_json(cfg: dict, n_docs, dims, iterations, objective, stop_reason,
     buf = C.create_string_buffer(n.value + 1)
     _check(lib, lib.sref_report_json(*args, buf, n.value + 1, C.byref(n)), "ref")
     return buf.value.decode()
+
+
+# ------------------------------------------------------------- vectorize ----
+def pack_texts(texts):
+    """Strings (or bytes) -> one UTF-8 byte array + int64 offsets."""
+    bs = [t.encode("utf-8") if isinstance(t, str) else bytes(t) for t in texts]
+    offs = np.zeros(len(bs) + 1, np.int64)
+    if bs:
+        offs[1:] = np.cumsum([len(b) for b in bs])
+    return b"".join(bs), offs
+
+
+def ref_vectorize(texts, stop_words=(), max_df=0.5):
+    """The reference's vectorize_corpus (corpus.cpp:101-134) on in-memory texts.
+
+    Returns dict(indptr, indices, values f64, kept, dropped, doc_freq, vocab,
+    n_docs, dims, seconds); kept / dropped are input positions (the shim uses
+    the decimal positions as doc ids)."""
+    lib = _load("ref")
+    text, offs = pack_texts(texts)
+    stext, soffs = pack_texts(list(stop_words))
+    h = _P()
+    _check(lib, lib.sref_vectorize(len(texts), text, offs, len(soffs) - 1, stext, soffs, float(max_df),
+                                   C.byref(h)), "ref")
+    try:
+        n_rows, nnz, nd = C.c_int64(), C.c_int64(), C.c_int64()
+        dims, n_docs = C.c_uint32(), C.c_uint32()
+        vb, secs = C.c_int64(), C.c_double()
+        lib.sref_vec_sizes(h, C.byref(n_rows), C.byref(nnz), C.byref(dims), C.byref(n_docs), C.byref(nd),
+                           C.byref(vb), C.byref(secs))
+        ptr = np.zeros(n_rows.value + 1, np.int64)
+        idx = np.zeros(max(nnz.value, 1), np.uint32)
+        val = np.zeros(max(nnz.value, 1), np.float64)
+        kept = np.zeros(max(n_rows.value, 1), np.int64)
+        dropped = np.zeros(max(nd.value, 1), np.int64)
+        dfq = np.zeros(max(dims.value, 1), np.uint32)
+        vt = C.create_string_buffer(max(vb.value, 1))
+        voff = np.zeros(dims.value + 1, np.int64)
+        lib.sref_vec_export(h, ptr, idx, val, kept, dropped, dfq, vt, voff)
+        raw = vt.raw[:vb.value]
+        vocab = [raw[voff[i]:voff[i + 1]].decode("utf-8", "surrogateescape") for i in range(dims.value)]
+        return {"indptr": ptr, "indices": idx[:nnz.value].astype(np.int32), "values": val[:nnz.value],
+                "kept": kept[:n_rows.value], "dropped": dropped[:nd.value], "doc_freq": dfq[:dims.value],
+                "vocab": vocab, "n_docs": int(n_docs.value), "dims": int(dims.value), "seconds": float(secs.value)}
+    finally:
+        lib.sref_vec_free(h)

@@ -18,6 +18,7 @@
 //   sref_run                  -> sskm::run (engine.hpp:148)
 //   sref_seed_kmeanspp        -> sskm::seed_kmeanspp (engine.hpp:74)
 //   sref_dot / sref_normalize -> sparse_vector.hpp:58-63
+//   sref_vectorize_*          -> sskm::vectorize_corpus (corpus.hpp:80-88) on in-memory texts
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -230,6 +231,78 @@ void* sref_synthetic_zipf(std::uint64_t n_docs, std::uint32_t vocab, double avg_
     });
     return rc == 0 ? m : nullptr;
 }
+
+// ------------------------------------------------------------- vectorize ---
+// vectorize_corpus (corpus.cpp:101-134) over texts given as one byte array with
+// offsets; doc ids are the decimal input indices, so kept / dropped ids map
+// back to positions. Vocabulary strings are exported in dim order.
+struct VecOut {
+    VectorizeResult r;
+    std::vector<std::string> terms;  // by dim
+    std::vector<std::int64_t> kept, dropped;
+    double seconds = 0.0;
+};
+
+int sref_vectorize(std::int64_t n_docs, const char* text, const std::int64_t* offs, std::int64_t n_stop,
+                   const char* stop_text, const std::int64_t* stop_offs, double max_df, void** out) {
+    *out = nullptr;
+    return guard([&] {
+        std::vector<std::pair<std::string, std::string>> docs;
+        docs.reserve(static_cast<std::size_t>(n_docs));
+        for (std::int64_t d = 0; d < n_docs; ++d)
+            docs.emplace_back(std::to_string(d), std::string(text + offs[d], text + offs[d + 1]));
+        StopWords stop;
+        for (std::int64_t w = 0; w < n_stop; ++w)
+            stop.insert(std::string(stop_text + stop_offs[w], stop_text + stop_offs[w + 1]));
+        auto* v = new VecOut();
+        try {
+            const auto t0 = std::chrono::steady_clock::now();
+            v->r = vectorize_corpus(docs, stop, max_df);
+            v->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            v->terms.resize(v->r.vocab.size());
+            for (const auto& [term, dim] : v->r.vocab.term_to_dim) v->terms[dim] = term;
+            for (const auto& id : v->r.matrix.doc_ids) v->kept.push_back(std::stoll(id));
+            for (const auto& id : v->r.dropped_doc_ids) v->dropped.push_back(std::stoll(id));
+        } catch (...) {
+            delete v;
+            throw;
+        }
+        *out = v;
+    });
+}
+
+void sref_vec_sizes(void* h, std::int64_t* n_rows, std::int64_t* nnz, std::uint32_t* dims, std::uint32_t* n_docs,
+                    std::int64_t* n_dropped, std::int64_t* vocab_bytes, double* seconds) {
+    auto* v = static_cast<VecOut*>(h);
+    *n_rows = static_cast<std::int64_t>(v->r.matrix.size());
+    *nnz = csr_nnz(v->r.matrix.vectors);
+    *dims = v->r.matrix.dims;
+    *n_docs = v->r.vocab.n_docs;
+    *n_dropped = static_cast<std::int64_t>(v->dropped.size());
+    std::int64_t b = 0;
+    for (const auto& t : v->terms) b += static_cast<std::int64_t>(t.size());
+    *vocab_bytes = b;
+    *seconds = v->seconds;
+}
+
+void sref_vec_export(void* h, std::int64_t* indptr, std::uint32_t* idx, double* val, std::int64_t* kept,
+                     std::int64_t* dropped, std::uint32_t* doc_freq, char* vocab_text, std::int64_t* vocab_off) {
+    auto* v = static_cast<VecOut*>(h);
+    csr_export(v->r.matrix.vectors, indptr, idx, val);
+    std::memcpy(kept, v->kept.data(), v->kept.size() * 8);
+    if (!v->dropped.empty()) std::memcpy(dropped, v->dropped.data(), v->dropped.size() * 8);
+    std::memcpy(doc_freq, v->r.vocab.doc_freq.data(), v->r.vocab.doc_freq.size() * 4);
+    std::int64_t o = 0;
+    vocab_off[0] = 0;
+    for (std::size_t d = 0; d < v->terms.size(); ++d) {
+        std::memcpy(vocab_text + o, v->terms[d].data(), v->terms[d].size());
+        o += static_cast<std::int64_t>(v->terms[d].size());
+        vocab_off[d + 1] = o;
+    }
+}
+
+void sref_vec_free(void* h) { delete static_cast<VecOut*>(h); }
+
 
 // ------------------------------------------------------------ primitives ---
 int sref_dot(std::int64_t na, const std::uint32_t* ia, const double* va, std::int64_t nb,

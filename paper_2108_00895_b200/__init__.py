@@ -18,6 +18,8 @@ from .api import (
     validate,
 )
 
+from .vectorize import VectorizeResult, vectorize_corpus, vectorize_texts
+
 _load_native()  # fail loudly at import if the native library is unusable
 
 __all__ = [
@@ -37,4 +39,7 @@ __all__ = [
     "cluster",
     "parse_mode",
     "validate",
+    "VectorizeResult",
+    "vectorize_corpus",
+    "vectorize_texts",
 ]

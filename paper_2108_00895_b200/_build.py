@@ -12,7 +12,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsskm_b200.so")
-SOURCES = ["engine.cu", "io.cpp"]
+SOURCES = ["engine.cu", "vectorize.cu", "io.cpp"]
 DEPS = SOURCES + sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp")))
 HEADER = os.path.join(os.path.dirname(PKG), "include", "sskm_b200.h")
 

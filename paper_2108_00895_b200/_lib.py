@@ -141,6 +141,16 @@ SIGNATURES = [
     ("sskm_postings_work", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     # extension (not in the reference): teacher-forcing of the NCC flags
     ("sskm_set_unchanged", C.c_int, [_P, _u8p]),
+    # GPU TF-IDF ingestion (vectorize_corpus, corpus.cpp:101-134)
+    ("sskm_vectorize", C.c_int, [C.c_int32, C.c_int64, C.c_char_p, _i64p, C.c_int64, C.c_char_p, _i64p, C.c_double,
+                                 C.POINTER(_P)]),
+    ("sskm_vec_sizes", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_uint32),
+                                 C.POINTER(C.c_uint32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("sskm_vec_export", C.c_int, [_P, _i64p, _i32p, _f64p, _i64p, _i64p, _u32p, C.c_char_p, _i64p]),
+    ("sskm_vec_stats", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                 C.POINTER(C.c_uint64)]),
+    ("sskm_vec_free", C.c_int, [_P]),
+    ("sskm_normalize_csr", C.c_int, [C.c_int32, C.c_int64, _i64p, _i32p, _f64p, _i64p, _i32p, _f64p]),
 ]
 
 _lib = None

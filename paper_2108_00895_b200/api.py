@@ -56,6 +56,7 @@ class CorpusMatrix:
         self.values = np.zeros(0, np.float32)
         self.dims = 0
         self.doc_ids: list = []
+        self.values64 = None  # exact fp64 weights when known (vectorize_corpus)
 
     @classmethod
     def from_csr(cls, indptr, indices, values, dims: int, doc_ids: Optional[Sequence[str]] = None):
@@ -88,7 +89,8 @@ class CorpusMatrix:
         if not 0 <= i < self.n_docs:
             raise IndexError(i)
         b, e = self.indptr[i], self.indptr[i + 1]
-        return SparseVector(self.indices[b:e], self.values[b:e].astype(np.float64), self.dims)
+        vals = self.values64[b:e] if self.values64 is not None else self.values[b:e].astype(np.float64)
+        return SparseVector(self.indices[b:e], vals, self.dims)
 
 
 @dataclass

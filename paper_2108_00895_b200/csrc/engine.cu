@@ -2469,6 +2469,13 @@ struct CachedEngine {
 std::mutex g_cache_mu;
 std::map<int, std::shared_ptr<CachedEngine>> g_engine_cache;
 
+}  // namespace
+
+namespace sskm_b200 {
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace sskm_b200
+
+namespace {
 template <class F>
 int guard(F&& f) {
     try {
