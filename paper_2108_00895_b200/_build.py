@@ -19,10 +19,17 @@ HEADER = os.path.join(os.path.dirname(PKG), "include", "sskm_b200.h")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O3,-fopenmp", "-lgomp",
+    "-Xcompiler", "-fPIC,-O3,-fopenmp",
     "-Xptxas", "-v",
-    "-shared", "-cudart", "static",
 ] + [f for f in os.environ.get("SSKM_NVCC_EXTRA", "").split() if f]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-lgomp"]
+OBJ = os.path.join(PKG, "build")  # objects (git-ignored): one per source, rebuilt when it or a header changed
+# headers each source includes (a source is recompiled only when one of its own changed)
+SRC_DEPS = {
+    "engine.cu": [f for f in DEPS if f.endswith(".cuh")],
+    "vectorize.cu": ["common.cuh"],
+    "io.cpp": [],
+}
 
 
 def _nvcc() -> str:
@@ -43,13 +50,30 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJ, exist_ok=True)
+
+    def compile_one(src: str) -> str:
+        obj = os.path.join(OBJ, src + ".o")
+        deps = [os.path.join(CSRC, src), HEADER] + [os.path.join(CSRC, h) for h in SRC_DEPS.get(src, [])]
+        if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps):
+            return obj
+        r = subprocess.run([_nvcc(), *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)], capture_output=True,
+                           text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed compiling {src}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    r = subprocess.run([_nvcc(), *LINK_FLAGS, "-o", LIB + ".tmp", *objs], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libsskm_b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libsskm_b200.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -303,16 +303,19 @@ constexpr int kRowBlock = 512;  // rows per partial in the column reductions
 // list raises *ovf: the host rebuilds); a new low value raises L_t. The lists
 // then hold exactly the entries >= thr of the new Cᵀ (plus zero pairs), and L_t
 // stays an upper bound on the row's low weights.
+// `hz` is the row's L_t bits, loaded with the round's other loads.
 __device__ __forceinline__ void hipost_maintain(uint4* __restrict__ hptr, uint2* __restrict__ pairs, uint32_t t,
-                                                uint32_t j, bool chg, float old, float cn, float thr,
+                                                uint32_t j, bool chg, float old, float cn, float thr, uint32_t hz,
                                                 unsigned int* ovf) {
     const bool oh = chg && old != 0.f && fabsf(old) >= thr;
     const bool nh = chg && cn != 0.f && fabsf(cn) >= thr;
     const bool lo = chg && !nh && cn != 0.f;
-    if (!__any_sync(0xFFFFFFFFu, oh || nh || lo)) return;
-    const uint4 h = hptr[t];
-    if (lo && fabsf(cn) > __uint_as_float(h.z)) atomicMax(&hptr[t].z, __float_as_uint(fabsf(cn)));
+    // the largest new low weight of the row's lanes against L_t (positive floats order as their bits)
+    const uint32_t lomax = __reduce_max_sync(0xFFFFFFFFu, lo ? __float_as_uint(fabsf(cn)) : 0u);
+    if (lomax > hz && (threadIdx.x & (kWarp - 1)) == 0) atomicMax(&hptr[t].z, lomax);
+    if (!__any_sync(0xFFFFFFFFu, oh || nh)) return;
     if (!(oh || nh)) return;
+    const uint4 h = hptr[t];
     const uint32_t sorted = h.w >> 16, cap = h.w & 0xFFFFu;
     const uint2* __restrict__ row = pairs + h.x;
     // binary search in the sorted part
@@ -342,7 +345,14 @@ __device__ __forceinline__ void hipost_maintain(uint4* __restrict__ hptr, uint2*
     }
 }
 
-__global__ void __launch_bounds__(128) write_groups_kernel(const long long* __restrict__ S, float* __restrict__ CT,
+#ifndef SSKM_WG_ROWS
+#define SSKM_WG_ROWS 4  // marked rows per round of write_groups_kernel (loads in flight per lane: 2 per row)
+#endif
+#ifndef SSKM_WG_MINB
+#define SSKM_WG_MINB 6
+#endif
+
+__global__ void __launch_bounds__(128, SSKM_WG_MINB) write_groups_kernel(const long long* __restrict__ S, float* __restrict__ CT,
                                                            uint64_t ld, uint32_t d, uint32_t k,
                                                            const uint8_t* __restrict__ touched,
                                                            const unsigned long long* __restrict__ Q,
@@ -350,6 +360,7 @@ __global__ void __launch_bounds__(128) write_groups_kernel(const long long* __re
                                                            unsigned int* __restrict__ nz, uint4* __restrict__ hptr,
                                                            uint2* __restrict__ pairs, float hthr,
                                                            unsigned int* hp_ovf) {
+    constexpr int R = SSKM_WG_ROWS;
     const int lane = threadIdx.x & (kWarp - 1);
     const uint32_t g = blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
     const uint32_t rb = blockIdx.y;
@@ -369,33 +380,40 @@ __global__ void __launch_bounds__(128) write_groups_kernel(const long long* __re
     const uint64_t wpr = ld >> 5;
     const uint32_t t0 = rb * kRowBlock, t1 = min(d, t0 + kRowBlock);
     double dr = 0.0;
+    // the bitmap words of the next 32 rows are loaded one step ahead
+    unsigned wr_n = t0 + lane < t1 ? nz[static_cast<uint64_t>(t0 + lane) * wpr + g] & amask : 0u;
     for (uint32_t tb = t0; tb < t1; tb += kWarp) {
-        const uint32_t tr = tb + lane;
-        const unsigned wr = tr < t1 ? nz[static_cast<uint64_t>(tr) * wpr + g] & amask : 0u;
+        const unsigned wr = wr_n;
+        {
+            const uint32_t trn = tb + kWarp + lane;
+            wr_n = trn < t1 ? nz[static_cast<uint64_t>(trn) * wpr + g] & amask : 0u;
+        }
         unsigned rows = __ballot_sync(0xFFFFFFFFu, wr != 0);
-        // four marked rows per round: all loads of a round before its stores
+        // R marked rows per round: all loads of a round before its stores
         while (rows) {
-            int r[4];
-            unsigned w[4];
+            int r[R];
+            unsigned w[R];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < R; ++q) {
                 r[q] = rows ? __ffs(rows) - 1 : -1;
                 if (rows) rows &= rows - 1;
                 w[q] = __shfl_sync(0xFFFFFFFFu, wr, r[q] < 0 ? 0 : r[q]);
             }
-            long long sv[4];
-            float old[4];
-            bool on[4];
+            long long sv[R];
+            float old[R];
+            uint32_t hz[R];
+            bool on[R];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < R; ++q) {
                 on[q] = r[q] >= 0 && (w[q] & lbit);
                 const uint64_t o = static_cast<uint64_t>(tb + r[q]) * ld + j;
                 sv[q] = on[q] ? __ldcs(S + o) : 0;
                 old[q] = on[q] ? CT[o] : 0.f;
+                hz[q] = (hthr > 0.f && r[q] >= 0) ? hptr[tb + r[q]].z : 0xFFFFFFFFu;
             }
-            float cn[4];
+            float cn[R];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < R; ++q) {
                 cn[q] = (!on[q] || sv[q] == 0) ? 0.f : static_cast<float>(static_cast<double>(sv[q]) * inv);
                 if (!on[q]) continue;
                 const uint64_t o = static_cast<uint64_t>(tb + r[q]) * ld + j;
@@ -406,9 +424,10 @@ __global__ void __launch_bounds__(128) write_groups_kernel(const long long* __re
             }
             if (hthr > 0.f) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < R; ++q) {
                     if (r[q] < 0) break;
-                    hipost_maintain(hptr, pairs, tb + r[q], j, on[q] && cn[q] != old[q], old[q], cn[q], hthr, hp_ovf);
+                    hipost_maintain(hptr, pairs, tb + r[q], j, on[q] && cn[q] != old[q], old[q], cn[q], hthr, hz[q],
+                                    hp_ovf);
                 }
             }
         }
