@@ -127,7 +127,9 @@ def workload_config(cfg, data, mode):
     return {"workload": f"{cfg.name}: N={data.n_docs}, d={cfg.dims}, k={cfg.k}, K_true={cfg.k_true}, "
                         f"mean len {cfg.mean_len:g} (sigma {cfg.sigma}), nnz={data.nnz}",
             "mode": mode, "init": "k distinct docs, numpy default_rng(0).choice",
-            "l2": "inputs larger than L2 (CSR 0.56 GB + Ct 1.07 GB + sums 2.1 GB >> 126 MB); no flush",
+            "l2": (lambda csr, ld: f"inputs larger than L2 (CSR {csr / 1e9:.2f} GB + Ct {cfg.dims * ld * 4 / 1e9:.2f} GB + "
+                   f"sums {cfg.dims * ld * 8 / 1e9:.1f} GB >> 126 MB); no flush")(
+                       data.nnz * 8 + (data.n_docs + 1) * 8, -(-cfg.k // 128) * 128),
             "parallelism": "doc-sharded"}
 
 

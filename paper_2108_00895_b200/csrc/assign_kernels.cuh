@@ -218,7 +218,8 @@ struct TileArgs {
     const float* val;
     const float* M;            // matrix scanned (Cᵀ, or the compact changed-column copy)
     uint64_t ld;               // row stride of M
-    uint32_t col0;             // first column of this tile
+    uint32_t col0;             // first column of this launch's tiles
+    uint32_t span;             // columns this launch covers (one tile of 32·V, or more: short work lists)
     uint32_t ncols;            // total columns of M (tile may be partial)
     const uint32_t* col_ids;   // cluster id per column of M (nullptr = identity)
     const uint32_t* order;     // work item -> document (nullptr = identity)
@@ -266,18 +267,24 @@ __global__ void __launch_bounds__(256, 2) assign_tile_kernel(TileArgs p) {
             arg = old_a;
         }
         {
-            double acc[V];
-            doc_tile_dots<V, U>(p.idx, p.val, beg, end, p.M, p.ld, p.col0, lane, acc);
+            // each lane keeps its own running (max, id) over the launch's tiles
+            // (the tie rule is a total order: any combination order gives the
+            // same winner), combined across the warp once
             double lb = best;
             uint32_t la = arg;
+            const uint32_t cend = min(p.ncols, p.col0 + p.span);
+            for (uint32_t c0 = p.col0; c0 < cend; c0 += 32u * V) {
+                double acc[V];
+                doc_tile_dots<V, U>(p.idx, p.val, beg, end, p.M, p.ld, c0, lane, acc);
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const uint32_t col = p.col0 + static_cast<uint32_t>(lane) * V + v;
-                if (col < p.ncols) {
-                    const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
-                    if (better(acc[v], id, lb, la)) {
-                        lb = acc[v];
-                        la = id;
+                for (int v = 0; v < V; ++v) {
+                    const uint32_t col = c0 + static_cast<uint32_t>(lane) * V + v;
+                    if (col < p.ncols) {
+                        const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
+                        if (better(acc[v], id, lb, la)) {
+                            lb = acc[v];
+                            la = id;
+                        }
                     }
                 }
             }
@@ -300,6 +307,69 @@ __global__ void __launch_bounds__(256, 2) assign_tile_kernel(TileArgs p) {
                 }
             }
         }
+    }
+}
+
+// Short work lists (what the screens leave: hundreds of documents against up to
+// 50,000 columns): a warp per (document, column span), so the scan's
+// parallelism comes from the columns too; each warp leaves its span's exact
+// (max, id) and a second kernel folds the spans into the running state with
+// the same total order.
+template <int V, int U>
+__global__ void __launch_bounds__(256, 2) assign_span_kernel(TileArgs p, uint32_t n_spans, double* __restrict__ part_s,
+                                                             uint32_t* __restrict__ part_a) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
+    const uint32_t sp = blockIdx.y;
+    const uint32_t c_beg = sp * p.span, c_end = min(p.ncols, c_beg + p.span);
+    for (int64_t w = static_cast<int64_t>(blockIdx.x) * nwarps + warp; w < p.n_work;
+         w += static_cast<int64_t>(gridDim.x) * nwarps) {
+        const int64_t i = p.order ? static_cast<int64_t>(__ldg(p.order + w)) : w;
+        const int64_t beg = __ldg(p.indptr + i), end = __ldg(p.indptr + i + 1);
+        double lb = -1e300;
+        uint32_t la = kNone;
+        for (uint32_t c0 = c_beg; c0 < c_end; c0 += 32u * V) {
+            double acc[V];
+            doc_tile_dots<V, U>(p.idx, p.val, beg, end, p.M, p.ld, c0, lane, acc);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const uint32_t col = c0 + static_cast<uint32_t>(lane) * V + v;
+                if (col < c_end) {
+                    const uint32_t id = p.col_ids ? __ldg(p.col_ids + col) : col;
+                    if (better(acc[v], id, lb, la)) {
+                        lb = acc[v];
+                        la = id;
+                    }
+                }
+            }
+        }
+        warp_argmax(lb, la);
+        if (lane == 0) {
+            part_s[w * n_spans + sp] = lb;
+            part_a[w * n_spans + sp] = la;
+        }
+    }
+}
+
+template <int INIT>
+__global__ void assign_span_reduce_kernel(TileArgs p, uint32_t n_spans, const double* __restrict__ part_s,
+                                          const uint32_t* __restrict__ part_a) {
+    static_assert(INIT != kInitNcc, "the NCC pass refreshes its baseline in the tile kernel");
+    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < p.n_work;
+         w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = p.order ? static_cast<int64_t>(p.order[w]) : w;
+        double best = INIT == kInitFull ? -2.0 : p.sims[i];  // engine.cpp:252-253; the rescan's running state
+        uint32_t arg = INIT == kInitFull ? 0u : p.a[i];
+        for (uint32_t sp = 0; sp < n_spans; ++sp) {
+            const double s = part_s[w * n_spans + sp];
+            const uint32_t a = part_a[w * n_spans + sp];
+            if (a != kNone && better(s, a, best, arg)) {
+                best = s;
+                arg = a;
+            }
+        }
+        p.a[i] = arg;
+        p.sims[i] = best;
     }
 }
 

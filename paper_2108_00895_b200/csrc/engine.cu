@@ -90,6 +90,8 @@ public:
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_SECOND_PASS")) second_pass_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_SECOND_RATIO")) second_pass_ratio_ = static_cast<float>(std::atof(e));
         if (const char* e = std::getenv("SSKM_KEEP_LISTS")) keep_lists_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_HASH")) hash_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_DEBUG")) debug_ = std::atoi(e) != 0;
@@ -1631,10 +1633,40 @@ private:
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
             1, std::min<int64_t>(static_cast<int64_t>(sms_) * blocks_per_sm_, ceil_div(n_work, 8))));
         dots_ += static_cast<uint64_t>(n_work) * ncols;  // every (document, column) pair, exact fp64
-        for (uint32_t c0 = 0; c0 < ncols; c0 += W) {
+        // long work lists go tile by tile (the tile's rows stay hot in L2 across
+        // the documents); short ones (the screens' leftovers) take every tile in
+        // one launch — hundreds of small launches cost more than the locality
+        const bool short_list = static_cast<uint64_t>(n_work) <= static_cast<uint64_t>(sms_) * 128;
+        if constexpr (INIT != kInitNcc) {
+            // short lists: a warp per (document, column span), spans folded after
+            const uint32_t tiles = static_cast<uint32_t>(ceil_div(ncols, W));
+            if (short_list && tiles > 1) {
+                const uint32_t want = static_cast<uint32_t>(
+                    std::min<int64_t>(64, std::max<int64_t>(1, ceil_div(static_cast<int64_t>(sms_) * 16, n_work))));
+                const uint32_t per = static_cast<uint32_t>(ceil_div(tiles, std::min(tiles, want)));
+                const uint32_t n_spans = static_cast<uint32_t>(ceil_div(tiles, per));
+                p.span = per * W;
+                span_s_.alloc(static_cast<size_t>(n_work) * n_spans);
+                span_a_.alloc(static_cast<size_t>(n_work) * n_spans);
+                const dim3 g2(static_cast<unsigned>(ceil_div(n_work, 8)), n_spans);
+                if (v == 4)
+                    assign_span_kernel<4, 16><<<g2, 256, 0, stream_>>>(p, n_spans, span_s_.p, span_a_.p);
+                else if (v == 2)
+                    assign_span_kernel<2, 16><<<g2, 256, 0, stream_>>>(p, n_spans, span_s_.p, span_a_.p);
+                else
+                    assign_span_kernel<1, 16><<<g2, 256, 0, stream_>>>(p, n_spans, span_s_.p, span_a_.p);
+                ++launches_;
+                launch(assign_span_reduce_kernel<INIT>, grid_for(n_work, 256), 256, p, n_spans, span_s_.p, span_a_.p);
+                CK_LAUNCH();
+                return;
+            }
+        }
+        const uint32_t span = short_list ? ncols : W;
+        for (uint32_t c0 = 0; c0 < ncols; c0 += span) {
             p.col0 = c0;
+            p.span = span;
             p.first = c0 == 0;
-            p.last = c0 + W >= ncols;
+            p.last = c0 + span >= ncols;
             launch_tile<INIT>(v, grid, p);
         }
         CK_LAUNCH();
@@ -1823,7 +1855,10 @@ private:
             pass_ms = static_cast<double>(ms) - build_ms_inner;
             screen_ms_ += pass_ms;
         }
-        const uint64_t n_list = n_work > 0 ? static_cast<uint64_t>(n_work) - std::min<uint64_t>(n_fb, n_work) : 0;
+        uint64_t n_fb2 = n_fb;  // documents left for the exact scan
+        if (hash && init == kInitFull && lists_here && second_pass_ && n_fb >= second_pass_min_)
+            n_fb2 = bound_second_pass(p, thr, n_fb);
+        const uint64_t n_list = n_work > 0 ? static_cast<uint64_t>(n_work) - std::min<uint64_t>(n_fb2, n_work) : 0;
         bstat_docs_ += n_list;
         bstat_pairs_ += ctr[1];
         dots_ += ctr[0] + ctr[3];  // exact fp64 dots: candidates and own-cluster dots
@@ -1858,10 +1893,13 @@ private:
             c.acc_hovf += static_cast<double>(ctr[6]);
             c.acc_work += static_cast<double>(n_work);
             if (!lists_here || ++c.passes >= kRebuildEvery) {
-                if (c.acc_hovf > 1e-4 * c.acc_work) {
+                // (a second pass makes a fallen-through document ~5 screens dear instead
+                // of an exact scan over every column: more of them are tolerated)
+                const bool sp = hash && init == kInitFull && second_pass_;
+                if (c.acc_hovf > (sp ? 3e-3 : 1e-4) * c.acc_work) {
                     c.target *= 0.7;
                     c.theta *= 1.3f;
-                } else if (c.acc_fb > 2e-3 * c.acc_work) {
+                } else if (c.acc_fb > (sp ? 2e-2 : 2e-3) * c.acc_work) {
                     c.target *= 1.4;
                     c.theta *= 0.7f;
                 }
@@ -1892,6 +1930,76 @@ private:
         CK(cudaMemcpyAsync(&tot, &scal_.p->n_moved, 8, cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
         return static_cast<double>(tot) / static_cast<double>(std::max<int64_t>(1, n_));
+    }
+
+    // Second pass of a hash-accumulator screen (configs 2 and 4). Documents the
+    // first pass could not settle — own similarity below the bound on the
+    // clusters they share no high entry with (Σ|x_t|·L_t is loose at the large θ
+    // that keeps k = 50,000 clusters' pairs within the tables), or a full table —
+    // used to take the exact scan over every column (c4: ~80k documents, half the
+    // iteration). They are screened again against lists at a much lower θ
+    // (tighter low-part bounds, ~4× the pairs) with 4096-slot tables; only what
+    // that leaves goes to the exact scan. The second lists are rebuilt per pass
+    // in their own buffers (one read of Cᵀ); the kept first-pass lists stay.
+    uint64_t bound_second_pass(const BoundArgs& p1, float thr1, uint64_t n_fb) {
+        constexpr int HT2 = 4096;
+        const float thr2 = std::max(1e-5f, thr1 * second_pass_ratio_);
+        exact2_.alloc(n_);
+        CK(cudaMemcpyAsync(exact2_.p, exact_.p, n_fb * sizeof(uint32_t), cudaMemcpyDeviceToDevice, stream_));
+        CK(cudaMemsetAsync(&scal_.p->n_exact, 0, 8, stream_));
+        CK(cudaMemsetAsync(bctr_.p, 0, 8 * sizeof(unsigned long long), stream_));
+        hptr2_.alloc(d_);
+        hpctr2_.alloc(2);
+        if (pairs2_.n == 0) pairs2_.alloc(std::max<size_t>(pairs_.n, 1u << 20));
+        CK(cudaMemsetAsync(hpctr2_.p, 0, 2 * sizeof(unsigned long long), stream_));
+        CK(cudaEventRecord(ev_[8], stream_));
+        const unsigned grid_b = static_cast<unsigned>(std::min<uint64_t>(ceil_div(d_, 8), static_cast<uint64_t>(sms_) * 32));
+        launch(hipost_build_kernel, grid_b, 256, static_cast<const float*>(ct_.p), static_cast<uint64_t>(ld_), d_, 0u, k_,
+               thr2, hptr2_.p, pairs2_.p, std::min<unsigned long long>(pairs2_.n, 0xFFFFFFFFull), hpctr2_.p,
+               hpctr2_.p + 1, 0);
+        CK_LAUNCH();
+        BoundArgs p = p1;
+        p.order = exact2_.p;
+        p.n_work = static_cast<int64_t>(n_fb);
+        p.n_work_dev = nullptr;
+        p.hptr = hptr2_.p;
+        p.pairs = pairs2_.p;
+        p.theta = static_cast<double>(thr2);
+        p.hp_overflow = hpctr2_.p + 1;
+        p.first = 1;
+        p.single_tile = 1;
+        p.last = 1;
+        CK(cudaEventRecord(ev_[6], stream_));
+        bound_launch_k(bound_screen_kernel<2048, kInitFull, HT2>, BoundSmem<2048, HT2>::per_warp, p);
+        CK(cudaEventRecord(ev_[7], stream_));
+        screen_launches_ += 1;
+        unsigned long long ctr[7] = {0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0};
+        CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(hp, hpctr2_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        if (hp[0] > pairs2_.n) pairs2_.alloc(static_cast<size_t>(std::min<unsigned long long>(hp[0], 0xFFFFFFFFull)) * 5 / 4 + 1);
+        float ms = 0.f, bms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
+        CK(cudaEventElapsedTime(&bms, ev_[8], ev_[6]));
+        screen_ms_ += ms;
+        second_ms_ += ms + bms;
+        second_docs_ += n_fb;
+        bstat_pairs_ += ctr[1];
+        dots_ += ctr[0] + ctr[3];
+        bstat_cand_ += ctr[0];
+        bstat_visits_ += ctr[2];
+        bstat_own_ += ctr[3];
+        bstat_doc_nnz_ += ctr[4];
+        bstat_cand_nnz_ += ctr[5];
+        if (debug_)
+            std::fprintf(stderr,
+                         "[sskm] bound second pass theta=%.5g work=%llu exact=%llu cand=%llu pairs=%llu hovf=%llu "
+                         "lists=%llu pairs (cap %zu, dropped=%llu) build %.2f ms screen %.2f ms\n",
+                         static_cast<double>(thr2), static_cast<unsigned long long>(n_fb),
+                         static_cast<unsigned long long>(hs_->n_exact), ctr[0], ctr[1], ctr[6], hp[0], pairs2_.n, hp[1],
+                         static_cast<double>(bms), static_cast<double>(ms));
+        return hs_->n_exact;
     }
 
     void bound_launch_hash(const BoundArgs& p, int init) {
@@ -2418,6 +2526,18 @@ private:
     double last_update_ms_ = 0.0;  // the last update's device time (θ tuning)
     uint64_t kpp_host_rounds_ = 0;  // k-means++ rounds the host had to replay (last seeding)
     bool skip_enabled_ = true;  // SSKM_SKIP=0: screen every document
+    // second pass of the hash screens (bound_second_pass)
+    bool second_pass_ = true;          // SSKM_SECOND_PASS=0: fallen-through documents go straight to the exact scan
+    float second_pass_ratio_ = 0.5f;  // θ of the second lists relative to the first pass's (measured on c4)
+    uint64_t second_pass_min_ = 512;   // fewer fallen-through documents than this: not worth the lists
+    DevBuf<uint4> hptr2_;
+    DevBuf<uint2> pairs2_;
+    DevBuf<unsigned long long> hpctr2_;
+    DevBuf<uint32_t> exact2_;
+    DevBuf<double> span_s_;   // exact scan of short lists: per (document, column span) maxima
+    DevBuf<uint32_t> span_a_;
+    double second_ms_ = 0.0;
+    uint64_t second_docs_ = 0;
     bool hash_enabled_ = true;  // SSKM_HASH=0: multi-tile passes instead of one hash-accumulator pass
     DevBuf<uint32_t> df_;       // document frequency per term (hash-pass θ)
     bool df_ready_ = false;
