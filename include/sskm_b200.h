@@ -84,7 +84,7 @@ typedef struct {
     double assign_kernel_ms;  /* device time of the assign kernels (screen, resolve, exact) */
     double screen_ms;         /* device time of the screen kernel launches only (bound or postings screen) */
     uint32_t screen_launches; /* screen launches in this assign (one per cluster tile) */
-    uint32_t reserved0;
+    uint32_t second_pass_docs; /* hash screens: documents the first pass left that a second pass (lower theta, larger tables) screened */
     double centroid_density;  /* nonzero fraction of the centroid tile last indexed (screen choice) */
     /* bound screen (the default screen after the seed assignment) */
     uint64_t bound_docs;       /* documents the bound screen resolved (summed over its passes) */

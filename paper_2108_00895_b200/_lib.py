@@ -58,7 +58,7 @@ class sskm_iteration_stats(C.Structure):
         ("assign_kernel_ms", C.c_double),
         ("screen_ms", C.c_double),
         ("screen_launches", C.c_uint32),
-        ("reserved0", C.c_uint32),
+        ("second_pass_docs", C.c_uint32),
         ("centroid_density", C.c_double),
         ("bound_docs", C.c_uint64),
         ("bound_pairs", C.c_uint64),

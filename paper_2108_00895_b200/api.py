@@ -119,7 +119,7 @@ class IterationStats:
     assign_kernel_ms: float = 0.0
     screen_ms: float = 0.0
     screen_launches: int = 0
-    reserved0: int = 0
+    second_pass_docs: int = 0
     centroid_density: float = 0.0
     bound_docs: int = 0
     bound_pairs: int = 0

@@ -92,6 +92,7 @@ public:
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SECOND_PASS")) second_pass_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SECOND_RATIO")) second_pass_ratio_ = static_cast<float>(std::atof(e));
+        if (const char* e = std::getenv("SSKM_SECOND_MIN")) second_pass_min_ = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("SSKM_KEEP_LISTS")) keep_lists_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_HASH")) hash_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_DEBUG")) debug_ = std::atoi(e) != 0;
@@ -1571,6 +1572,8 @@ private:
         dots_ = 0;
         skip_docs_ = 0;
         skip_ms_ = 0.0;
+        second_docs_ = 0;
+        second_ms_ = 0.0;
         CK(cudaMemcpyAsync(a_start_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
         CK(cudaMemcpyAsync(sims_start_.p, sims_.p, n_ * 8, cudaMemcpyDeviceToDevice, stream_));
     }
@@ -2419,6 +2422,7 @@ private:
         st->bound_visits = bstat_visits_;
         st->bound_own_dots = bstat_own_;
         st->skip_docs = skip_docs_;
+        st->second_pass_docs = static_cast<uint32_t>(std::min<uint64_t>(second_docs_, 0xFFFFFFFFull));
         st->skip_ms = skip_ms_;
     }
 
@@ -2695,6 +2699,7 @@ void step(Engine& e, sskm_iteration_stats* st) {
     st->bound_visits = a.bound_visits;
     st->bound_own_dots = a.bound_own_dots;
     st->skip_docs = a.skip_docs;
+    st->second_pass_docs = a.second_pass_docs;
     st->skip_ms = a.skip_ms;
     st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

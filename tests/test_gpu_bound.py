@@ -107,6 +107,39 @@ def test_bound_default_teacher_forced_against_oracle():
         assert np.array_equal(rs, s), it
 
 
+@pytest.mark.parametrize("case", ["two_tiles", "five_tiles"])
+@pytest.mark.parametrize("mode", ["baseline", "ncc"])
+def test_hash_second_pass_is_exact(case, mode, monkeypatch):
+    """Hash-accumulator passes (k > 2048): documents the first pass cannot settle
+    are screened again at a lower θ with larger tables before the exact scan
+    (bound_second_pass); with or without that pass, and for any θ ratio, the
+    trajectory is the same bit for bit. θ = 0.1 makes many documents fall
+    through; the leftovers take the span-parallel exact scan."""
+    m, k = CASES[case]()
+    seeds = np.random.default_rng(0).choice(m.n_docs, k, replace=False)
+    monkeypatch.setenv("SSKM_THETA", "0.1")
+    monkeypatch.setenv("SSKM_SECOND_PASS", "0")
+    ref, _ = trajectory(m, k, seeds, mode, 4)
+    monkeypatch.setenv("SSKM_SECOND_PASS", "1")
+    monkeypatch.setenv("SSKM_SECOND_MIN", "1")
+    ran = 0
+    for ratio in ("0.5", "0.05"):
+        monkeypatch.setenv("SSKM_SECOND_RATIO", ratio)
+        eng = P.Engine(0)
+        eng.upload(m)
+        eng.configure(k, mode=mode, conv_sq_dist=1e-300, max_iters=4)
+        eng.init_from_seeds(seeds)
+        out = []
+        for _ in range(4):
+            st = eng.step()
+            ran += st.second_pass_docs
+            a, s, _ = eng.get_state()
+            out.append((a.copy(), s.copy(), st.dot_products, st.n_reassigned))
+        assert_same(ref, out, f"second pass ratio={ratio}")
+    if mode == "baseline":
+        assert ran > 0  # the second pass did run
+
+
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_postings_overflow_stays_exact(case, monkeypatch):
     """A high-postings buffer too small for the first bound pass: single-tile
