@@ -28,6 +28,8 @@
 // between the screen, the candidate dots and the exact scan).
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "assign_kernels.cuh"
 
 namespace sskm_b200 {
@@ -36,6 +38,8 @@ namespace sskm_b200 {
 #define SSKM_BOUND_MINB 4  // resident 256-thread blocks per SM the register budget is cut for
 #endif
 
+constexpr int kUbGroups = 32;            // drift bound: clusters grouped by id mod 32 (one group per lane)
+constexpr unsigned short kHalfInf = 0x7C00u;
 constexpr float kFixScale = 0x1p30f;    // fixed-point products: q = rn(p · 2^30)
 constexpr double kFixUnit = 0x1p-30;
 
@@ -75,10 +79,11 @@ struct BoundArgs {
     unsigned long long* n_visits;    // documents visited, summed over tiles (roofline bytes)
     unsigned long long* n_cand_nnz;  // nonzeros of the candidate dots (centroid values gathered)
     unsigned long long* n_own;       // own dots computed in the screen
-    // drift bound (single-tile full-scan passes; nullptr otherwise): per
-    // document a certified upper bound on its similarity to every cluster other
-    // than its own, and the iteration it holds for (skip_kernel)
-    float* ub;
+    // drift bound (full-scan passes over every document; nullptr otherwise):
+    // per document and cluster group g (cluster id mod 32) a certified upper
+    // bound on its similarity to every cluster of the group other than its
+    // own (fp16, rounded up), and the iteration it holds for (skip_kernel)
+    __half* ub;
     uint32_t* ub_it;
     uint32_t iter;
     const unsigned long long* n_work_dev;  // work-list length on the device (overrides n_work)
@@ -483,14 +488,47 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             // no touched cluster can reach best: nothing to evaluate
             const uint32_t count =
                 static_cast<double>(accmax) * kFixUnit + bx >= best ? (dense ? (HT > 0 ? kSlots : p.kt) : ntouch) : 0u;
-            if (p.ub && lane == 0) {
-                // every other cluster j of this tile: s_j <= acc_j·2^-30 + bx <=
-                // accmax·2^-30 + bx (the own cluster's pairs were never
-                // accumulated); the maximum over the tiles; withdrawn below if
-                // the document moves (its new cluster's pairs were)
-                const float u = __double2float_ru(static_cast<double>(accmax) * kFixUnit + bx);
-                p.ub[i] = first ? u : fmaxf(p.ub[i], u);
-                if (first) p.ub_it[i] = p.iter;
+            if (p.ub) {
+                // every other cluster j of this tile: s_j <= acc_j·2^-30 + bx (the own
+                // cluster's pairs were never accumulated; untouched clusters have
+                // acc = 0). Lane g keeps the largest accumulator of the clusters
+                // with id ≡ g (mod 32): the group's bound, the maximum over the
+                // tiles; withdrawn below if the document moves (its new cluster's
+                // pairs were accumulated). The fold buffer is free until the
+                // candidate dots.
+                const uint32_t s_gm = sb + SM::o_fold;
+                sm_st_u32(s_gm + 4u * lane, 0u);
+                __syncwarp();
+                if (dense) {
+                    int m = 0;
+                    for (int c = lane; c < kSlots; c += kWarp) {
+                        const int v = static_cast<int>(sm_ld_u32(s_acc + 4u * c));
+                        if constexpr (HT > 0) {
+                            const uint32_t key = sm_ld_u32(s_key + 4u * c);
+                            if (key != 0 && v > 0)
+                                asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * ((key - 1u) & 31u)), "r"(v));
+                        } else {
+                            m = max(m, v);  // column c0 + c, c0 a multiple of 32: group = lane
+                        }
+                    }
+                    if constexpr (HT == 0) sm_st_u32(s_gm + 4u * lane, static_cast<uint32_t>(m));
+                } else {
+                    for (uint32_t kk = lane; kk < ntouch; kk += kWarp) {
+                        const uint32_t jl = sm_ld_u16(s_tl + 2u * kk);
+                        const int v = static_cast<int>(sm_ld_u32(s_acc + 4u * jl));
+                        uint32_t col = p.c0 + jl;
+                        if constexpr (HT > 0) col = sm_ld_u32(s_key + 4u * jl) - 1u;
+                        if (v > 0) asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * (col & 31u)), "r"(v));
+                    }
+                }
+                __syncwarp();
+                const int gmax = static_cast<int>(sm_ld_u32(s_gm + 4u * lane));
+                __half u = __float2half_ru(__double2float_ru(static_cast<double>(gmax) * kFixUnit + bx));
+                __half* ug = p.ub + static_cast<uint64_t>(i) * kUbGroups + lane;
+                if (!first) u = __hmax(u, *ug);
+                *ug = u;
+                if (first && lane == 0) p.ub_it[i] = p.iter;
+                __syncwarp();  // the fold buffer goes back to the candidate dots
             }
             uint32_t c_gid = 0;   // this lane's pending candidate
             double c_ub = -1e300;
@@ -573,12 +611,13 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             }
             drain(true);
             if (lane == 0) {
-                if (p.ub && p.last && arg != p.a_start[i]) p.ub[i] = __int_as_float(0x7f800000);
+                if (p.ub && p.last && arg != p.a_start[i])
+                    p.ub[static_cast<uint64_t>(i) * kUbGroups] = __ushort_as_half(kHalfInf);
                 p.a[i] = arg;
                 p.sims[i] = best;
             }
         } else if (first && p.ub && lane == 0) {
-            p.ub[i] = __int_as_float(0x7f800000);  // exact scan: no bound
+            p.ub[static_cast<uint64_t>(i) * kUbGroups] = __ushort_as_half(kHalfInf);  // exact scan: no bound
         }
         // clear the touched accumulators
         __syncwarp();
@@ -608,31 +647,38 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
 }
 
 // Drift bound (full-scan passes). The bound screen leaves, for every document
-// that kept its cluster a, U_i >= s_ij for every j != a: the reference's fp64
-// dot against the centroids of that iteration t_s. Centroid columns then move
-// by δ_j = ||c_j^new − c_j^old||_2 per update, so in real arithmetic x·c_j grows
-// by at most ||x||_2·Σδ, and
-//   s_ij(t) <= U_i + ||x||_2·(D(t) − D(t_s)) + 2·γ64(n)·||x||_2·cmax,
-// D = the running sum of the updates' max_j δ_j (the two γ64 terms convert
-// between the reference's rounded dots and real ones at t_s and at t). A
-// document whose own column is bit-identical to the previous iteration's
-// (`same`: its cached similarity is exact) and whose cached own similarity
-// exceeds that bound strictly keeps its cluster with exactly the reference's
-// result — no other cluster can win or tie — and needs no screen. Every other
-// document goes to a work list for the bound screen, ascending within each
-// block's 1024-document range. (Documents whose own column moved need an own
-// dot in any case; the screen computes it fused with its loads, far cheaper
-// than a separate pass — measured.) The paper's use of centroid stability
-// (unchanged clusters, engine.cpp:268-275) is the ε = 0 case of this bound.
+// that kept its cluster a and every cluster group g (cluster id mod 32),
+// U_ig >= s_ij for every j != a of the group: the reference's fp64 dot against
+// the centroids of that iteration t_s. Centroid columns then move by
+// δ_j = ||c_j^new − c_j^old||_2 per update, so in real arithmetic x·c_j grows
+// by at most ||x||_2·Σδ_j, and
+//   s_ij(t) <= U_ig + ||x||_2·(D_g(t) − D_g(t_s)) + 2·γ64(n)·||x||_2·cmax,
+// D_g = the running sum of the updates' max δ_j over the group's clusters (the
+// two γ64 terms convert between the reference's rounded dots and real ones at
+// t_s and at t). One global D (the maximum over all clusters) is dominated by
+// the few clusters that move a lot — on c1 the largest drift is 10-50× the
+// 90th percentile — and would hold every document hostage to them; per group,
+// an unstable cluster only weakens its own group's bound, which is far from
+// most documents' similarity anyway. A document whose own column is
+// bit-identical to the previous iteration's (`same`: its cached similarity is
+// exact) and whose cached own similarity exceeds every group's bound strictly
+// keeps its cluster with exactly the reference's result — no other cluster can
+// win or tie — and needs no screen. Every other document goes to a work list
+// for the bound screen, ascending within each block's 1024-document range.
+// (Documents whose own column moved need an own dot in any case; the screen
+// computes it fused with its loads — measured: neither a separate own-dot pass
+// nor an own-dot-first path inside the screen pays, most such documents fail
+// the test.) The paper's use of centroid stability (unchanged clusters,
+// engine.cpp:268-275) is the ε = 0 case of this bound.
 struct SkipArgs {
     const int64_t* indptr;
     int64_t n;
     const uint32_t* a;
     const double* sims;
     const uint8_t* same;
-    const float* ub;
+    const __half* ub;        // [n][32]
     const uint32_t* ub_it;
-    const double* dcum;  // D by iteration
+    const double* dcum;      // D_g by iteration: [iteration][32]
     uint32_t iter;
     const float2* xb;
     double cmax;
@@ -643,15 +689,47 @@ struct SkipArgs {
 
 constexpr int kSkipDocsPerBlock = 1024;
 
+// Per-group running drift: D_g(it) = D_g(it − 1) + sqrt(max_{j ≡ g} drift²_j)·(1 + 1e-9)
+// (0 growth when the update cannot be followed: the host then invalidates the
+// bounds). One block of 32 warps, warp g = group g.
+__global__ void __launch_bounds__(1024) group_drift_kernel(const double* __restrict__ drift_sq, uint32_t k, int ok,
+                                                           double* __restrict__ dcum, uint32_t iter) {
+    const int lane = threadIdx.x & (kWarp - 1), g = threadIdx.x / kWarp;
+    double m = 0.0;
+    if (ok)
+        for (uint32_t j = g + kUbGroups * lane; j < k; j += kUbGroups * kWarp) m = fmax(m, drift_sq[j]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
+    if (lane == 0) {
+        const double prev = iter > 0 ? dcum[static_cast<uint64_t>(iter - 1) * kUbGroups + g] : 0.0;
+        // a NaN or negative drift cannot be followed either: the host checks the maximum
+        dcum[static_cast<uint64_t>(iter) * kUbGroups + g] = prev + (ok && m > 0.0 ? sqrt(m) * (1.0 + 1e-9) : 0.0);
+    }
+}
+
+constexpr int kSkipHist = 64;  // iterations of group drift kept in shared memory (older bounds read global memory)
+
+// A thread per document (four consecutive documents each): its 32 group
+// bounds arrive as four 16-byte loads; the growth factors
+// G[t][g] = (D_g(now) − D_g(t))·(1 + 1e-9), rounded up to fp32, of the last
+// kSkipHist iterations sit in shared memory (row stride 33: lanes whose bounds
+// date from different iterations hit different banks).
 __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
+    __shared__ float G[kSkipHist][kUbGroups + 1];
     __shared__ uint32_t wsum[8];
     __shared__ unsigned long long base_sm;
     const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x / kWarp, nwarps = blockDim.x / kWarp;
+    const uint32_t t_lo = p.iter >= static_cast<uint32_t>(kSkipHist) ? p.iter - (kSkipHist - 1) : 0u;
+    const double* __restrict__ dnow = p.dcum + static_cast<uint64_t>(p.iter) * kUbGroups;
+    for (uint32_t e = threadIdx.x; e < (p.iter - t_lo + 1) * kUbGroups; e += blockDim.x) {
+        const uint32_t r = e / kUbGroups, g = e % kUbGroups;
+        G[r][g] = __double2float_ru((dnow[g] - p.dcum[static_cast<uint64_t>(t_lo + r) * kUbGroups + g]) * (1.0 + 1e-9));
+    }
+    __syncthreads();
     const int64_t d0 = static_cast<int64_t>(blockIdx.x) * kSkipDocsPerBlock;
     const int cnt = static_cast<int>(min(static_cast<int64_t>(kSkipDocsPerBlock), p.n - d0));
     constexpr int kPer = kSkipDocsPerBlock / 256;
     const int my0 = threadIdx.x * kPer;  // four consecutive documents per thread
-    const double dnow = p.dcum[p.iter];
     bool kp[kPer];
     uint32_t mine = 0, out = 0;
 #pragma unroll
@@ -660,12 +738,43 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
         if (my0 + q >= cnt) continue;
         const int64_t i = d0 + my0 + q;
         kp[q] = true;
-        const float u = p.ub[i];
-        if (u != __int_as_float(0x7f800000) && p.same[p.a[i]]) {
-            const float2 xb = p.xb[i];
+        if (p.same[p.a[i]]) {
+            const uint4* __restrict__ row = reinterpret_cast<const uint4*>(p.ub + static_cast<uint64_t>(i) * kUbGroups);
+            uint4 w[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) w[v] = row[v];
+            const uint32_t its = p.ub_it[i];
+            const float x2 = p.xb[i].y;
+            float bmax = 0.f;  // every rounding upward; +inf marks a withdrawn bound
+            auto fold2 = [&](uint32_t hh, float g0, float g1) {
+                const __half2 h2 = *reinterpret_cast<const __half2*>(&hh);
+                bmax = fmaxf(bmax, __fmaf_ru(x2, g0, __low2float(h2)));
+                bmax = fmaxf(bmax, __fmaf_ru(x2, g1, __high2float(h2)));
+            };
+            if (its >= t_lo && its <= p.iter) {
+                const float* __restrict__ gr = G[its - t_lo];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    fold2(w[v].x, gr[8 * v + 0], gr[8 * v + 1]);
+                    fold2(w[v].y, gr[8 * v + 2], gr[8 * v + 3]);
+                    fold2(w[v].z, gr[8 * v + 4], gr[8 * v + 5]);
+                    fold2(w[v].w, gr[8 * v + 6], gr[8 * v + 7]);
+                }
+            } else if (its > p.iter) {
+                bmax = __int_as_float(0x7f800000);  // not a stamp of this run: no bound
+            } else {  // a bound older than the shared history
+                const double* __restrict__ dt = p.dcum + static_cast<uint64_t>(its) * kUbGroups;
+                auto gg = [&](int g) { return __double2float_ru((dnow[g] - dt[g]) * (1.0 + 1e-9)); };
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    fold2(w[v].x, gg(8 * v + 0), gg(8 * v + 1));
+                    fold2(w[v].y, gg(8 * v + 2), gg(8 * v + 3));
+                    fold2(w[v].z, gg(8 * v + 4), gg(8 * v + 5));
+                    fold2(w[v].w, gg(8 * v + 6), gg(8 * v + 7));
+                }
+            }
             const double nn = static_cast<double>(p.indptr[i + 1] - p.indptr[i]);
-            const double grow = static_cast<double>(xb.y) * (dnow - p.dcum[p.ub_it[i]]) * (1.0 + 1e-9);
-            const double b = static_cast<double>(u) + grow + 2.0 * gamma_ub(nn, 0x1p-53) * xb.y * p.cmax * (1.0 + 1e-12) +
+            const double b = static_cast<double>(bmax) + 2.0 * gamma_ub(nn, 0x1p-53) * x2 * p.cmax * (1.0 + 1e-12) +
                              nn * 0x1p-126;
             kp[q] = !(p.sims[i] > b);
         }

@@ -90,6 +90,7 @@ public:
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_REBUILD_LATE")) rebuild_late_ = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SSKM_SECOND_PASS")) second_pass_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SECOND_RATIO")) second_pass_ratio_ = static_cast<float>(std::atof(e));
         if (const char* e = std::getenv("SSKM_SECOND_MIN")) second_pass_min_ = std::strtoull(e, nullptr, 10);
@@ -518,6 +519,7 @@ public:
         CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
         ub_valid_ = false;
         iteration_ = 0;
+        dcum_rows_ = 0;
         have_cc_ = false;
         state_ = true;
         CK(cudaStreamSynchronize(stream_));
@@ -1338,11 +1340,10 @@ private:
         pptr_.alloc(d_ + 1);
         moves_.alloc(2 * static_cast<size_t>(k_));
         // drift bound (skip_kernel)
-        ub_.alloc(n_);
+        ub_.alloc(static_cast<size_t>(n_) * kUbGroups);
         ub_it_.alloc(n_);
         skip_list_.alloc(n_);
         skip_ctr_.alloc(4);
-        if (dcum_.n == 0) dcum_.alloc(4096);
         btake_.alloc(n_);
         bctr_.alloc(8);
         hptr_.alloc(d_);
@@ -1382,6 +1383,7 @@ private:
         reset_sums();
         CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
         iteration_ = 0;
+        dcum_rows_ = 0;
         have_cc_ = false;
         state_ = true;
     }
@@ -1509,6 +1511,7 @@ private:
         CK(cudaEventRecord(ev_[1], stream_));  // end of the update (timed by the caller)
         pull_scalars();
         const uint32_t n_rec = hs_->n_rec;
+        last_n_rec_ = n_rec;
         if (hs_->zero_flag) throw InvalidArgument("cannot normalize zero vector");
         if (hs_->hp_ovf) hp_valid_ = false;
         n_unchanged_ = hs_->n_unchanged;
@@ -1527,25 +1530,31 @@ private:
         st->n_recomputed = n_rec;
     }
 
-    // Running sum D of the updates' max column drift (the drift bound's growth,
-    // skip_kernel); an update the bounds cannot follow (iteration 1, an
-    // empty-cluster repair) invalidates them until the next full screen.
+    // Running sums D_g of the updates' max column drift per cluster group (the
+    // drift bound's growth, skip_kernel), accumulated on the device from the
+    // update's per-column drift; an update the bounds cannot follow (iteration
+    // 1, an empty-cluster repair) adds nothing and invalidates them until the
+    // next full screen.
     void advance_drift(double max_sq_drift) {
-        if (dcum_h_.empty()) dcum_h_.push_back(0.0);
-        while (dcum_h_.size() <= iteration_) dcum_h_.push_back(dcum_h_.back());
         const bool ok = iteration_ >= 2 && repaired_.empty() && max_sq_drift >= 0.0 && std::isfinite(max_sq_drift);
-        const double step = ok ? std::sqrt(max_sq_drift) * (1.0 + 1e-9) : 0.0;
-        dcum_h_[iteration_] = (iteration_ > 0 ? dcum_h_[iteration_ - 1] : 0.0) + step;
         if (!ok) ub_valid_ = false;
-        if (dcum_.n < dcum_h_.size()) {
-            dcum_.alloc(std::max<size_t>(4096, 2 * dcum_h_.size()));
-            CK(cudaMemcpyAsync(dcum_.p, dcum_h_.data(), dcum_h_.size() * sizeof(double), cudaMemcpyHostToDevice,
-                               stream_));
-        } else {
-            CK(cudaMemcpyAsync(dcum_.p + iteration_, &dcum_h_[iteration_], sizeof(double), cudaMemcpyHostToDevice,
-                               stream_));
+        const size_t rows = static_cast<size_t>(iteration_) + 1;
+        if (dcum_.n < rows * kUbGroups) {  // grow, keeping the history (bounds refer to their own iteration's row)
+            DevBuf<double> bigger;
+            bigger.alloc(std::max<size_t>(4096, 2 * rows) * kUbGroups);
+            CK(cudaMemsetAsync(bigger.p, 0, bigger.n * sizeof(double), stream_));
+            if (dcum_.n) CK(cudaMemcpyAsync(bigger.p, dcum_.p, dcum_.n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+            CK(cudaStreamSynchronize(stream_));
+            std::swap(dcum_.p, bigger.p);
+            std::swap(dcum_.n, bigger.n);
         }
-        CK(cudaStreamSynchronize(stream_));  // the host vector may reallocate before the next copy
+        // rows between the last written one and this one (engines driven through
+        // update_apply after a reset) carry the previous sums forward
+        for (uint32_t it = dcum_rows_; it < iteration_; ++it)
+            launch(group_drift_kernel, 1, 1024, static_cast<const double*>(drift_.p), k_, 0, dcum_.p, it);
+        launch(group_drift_kernel, 1, 1024, static_cast<const double*>(drift_.p), k_, ok ? 1 : 0, dcum_.p, iteration_);
+        CK_LAUNCH();
+        dcum_rows_ = iteration_ + 1;
     }
 
     void ensure_cc() {
@@ -1691,7 +1700,7 @@ private:
         // place by the column rewrite; rebuilt (and θ re-tuned) every
         // kRebuildEvery assigns, or when they were invalidated
         const bool lists_here = ncols <= KT && M == ct_.p;
-        const bool reuse = keep_lists_ && lists_here && hp_valid_ && assigns_since_build_ + 1 < kRebuildEvery &&
+        const bool reuse = keep_lists_ && lists_here && hp_valid_ && assigns_since_build_ + 1 < rebuild_every() &&
                            (theta_adapt_ || theta_ == hp_theta_);
         if (hash && theta_adapt_ && !hash_theta_started_) {  // the first hash pass of this configuration
             for (auto& q : tctl_) q.theta = std::max(q.theta, hash_theta0_);
@@ -1739,12 +1748,12 @@ private:
         const bool full_cover = init == kInitFull && order == nullptr && col_ids == nullptr && n_work == n_;
         bool skipped = false;
         if (full_cover) {
-            ub_.alloc(n_);
+            ub_.alloc(static_cast<size_t>(n_) * kUbGroups);
             ub_it_.alloc(n_);
             p.ub = ub_.p;
             p.ub_it = ub_it_.p;
             p.iter = iteration_;
-            if (skip_enabled_ && ub_valid_ && p.same && iteration_ < dcum_h_.size()) {
+            if (skip_enabled_ && ub_valid_ && p.same && iteration_ < dcum_rows_) {
                 skip_list_.alloc(n_);
                 skip_ctr_.alloc(4);
                 CK(cudaMemsetAsync(skip_ctr_.p, 0, 4 * sizeof(unsigned long long), stream_));
@@ -1895,7 +1904,7 @@ private:
             c.acc_fb += static_cast<double>(n_fb - std::min<uint64_t>(n_fb, ctr[6]));
             c.acc_hovf += static_cast<double>(ctr[6]);
             c.acc_work += static_cast<double>(n_work);
-            if (!lists_here || ++c.passes >= kRebuildEvery) {
+            if (!lists_here || ++c.passes >= rebuild_every()) {
                 // (a second pass makes a fallen-through document ~5 screens dear instead
                 // of an exact scan over every column: more of them are tolerated)
                 const bool sp = hash && init == kInitFull && second_pass_;
@@ -2513,14 +2522,20 @@ private:
     double bstat_theta_ = 0.0;
     uint64_t dots_ = 0;
     // drift bound (skip_kernel)
-    DevBuf<float> ub_;
+    DevBuf<__half> ub_;        // [n][32]: per document and cluster group
     DevBuf<uint32_t> ub_it_, skip_list_;
     DevBuf<double> dcum_;
     DevBuf<unsigned long long> skip_ctr_;
-    std::vector<double> dcum_h_;
+    uint32_t dcum_rows_ = 0;   // rows of dcum_ ([iteration][32]) written so far
     bool ub_valid_ = false;     // every document's bound is valid for the current assignments
     // high postings kept across passes (single cluster tile over Cᵀ)
     static constexpr uint32_t kRebuildEvery = 4;
+    uint32_t rebuild_late_ = 16;  // SSKM_REBUILD_LATE: the period once few columns change per update
+    // The kept lists are rebuilt for fresh, tight L_t (maintenance only ever
+    // raises them) and to re-tune θ: every 4 assigns while the centroids still
+    // move a lot, less often once an update rewrites under a third of the columns.
+    uint32_t rebuild_every() const { return last_n_rec_ * 3 < k_ ? rebuild_late_ : kRebuildEvery; }
+    uint32_t last_n_rec_ = 0xFFFFFFFFu / 4;
     bool hp_valid_ = false;     // hptr_/pairs_ hold exactly Cᵀ's entries >= hp_theta_
     bool keep_lists_ = true;    // SSKM_KEEP_LISTS=0: rebuild the high postings every assign
     float theta0_ = 0.004f, hash_theta0_ = 0.02f;

@@ -348,11 +348,8 @@ __device__ __forceinline__ void hipost_maintain(uint4* __restrict__ hptr, uint2*
 #ifndef SSKM_WG_ROWS
 #define SSKM_WG_ROWS 4  // marked rows per round of write_groups_kernel (loads in flight per lane: 2 per row)
 #endif
-#ifndef SSKM_WG_MINB
-#define SSKM_WG_MINB 6
-#endif
 
-__global__ void __launch_bounds__(128, SSKM_WG_MINB) write_groups_kernel(const long long* __restrict__ S, float* __restrict__ CT,
+__global__ void __launch_bounds__(128) write_groups_kernel(const long long* __restrict__ S, float* __restrict__ CT,
                                                            uint64_t ld, uint32_t d, uint32_t k,
                                                            const uint8_t* __restrict__ touched,
                                                            const unsigned long long* __restrict__ Q,
