@@ -126,11 +126,9 @@ public:
         cudaSetDevice(device_);
         cudaStreamSynchronize(stream_);
         for (auto& e : ev_) cudaEventDestroy(e);
+        if (stage_[0]) cudaFreeHost(stage_[0]);  // one allocation, two halves
         for (int b = 0; b < 2; ++b)
-            if (stage_[b]) {
-                cudaFreeHost(stage_[b]);
-                if (stage_ev_[b]) cudaEventDestroy(stage_ev_[b]);
-            }
+            if (stage_ev_[b]) cudaEventDestroy(stage_ev_[b]);
         for (auto& e : user_ev_) cudaEventDestroy(e);
         cudaStreamDestroy(stream_);
         if (hs_) cudaFreeHost(hs_);
@@ -162,22 +160,33 @@ public:
     void synchronize() { CK(cudaStreamSynchronize(stream_)); }
 
     // ------------------------------------------------------------ corpus --
-    // Host -> device copy of a large pageable buffer through two pinned 64 MB
-    // staging buffers: the host copies (parallel threads) into one while the
-    // other's DMA runs. The driver's own pageable path runs at ~8 GB/s here.
+    // Host -> device copy of a large pageable buffer through two pinned 8 MB
+    // staging buffers (halves of one allocation): the host copies (parallel
+    // threads, ~43 GB/s) into one while the other's DMA runs. The driver's own
+    // pageable path runs at ~8-10 GB/s here. One allocation of 16 MB: page-
+    // locking costs ~6 ms per call plus ~0.1-0.4 ms per MB on this host — the
+    // two 64 MB buffers of round 1 cost 60-80 ms per engine, more than the
+    // 0.56 GB c1 upload itself.
     void h2d(void* dst, const void* src, size_t bytes) {
-        constexpr size_t kChunk = size_t(64) << 20;
-        for (int b = 0; b < 2 && bytes >= (size_t(8) << 20) && !stage_failed_; ++b)
-            if (!stage_[b]) {
-                if (cudaMallocHost(&stage_[b], kChunk) != cudaSuccess) {  // no pinned memory: pageable copies
-                    (void)cudaGetLastError();
-                    stage_[b] = nullptr;
-                    stage_failed_ = true;
-                    break;
+        constexpr size_t kChunk = size_t(8) << 20;
+        if (bytes >= (size_t(8) << 20) && !stage_failed_ && !stage_[0]) {
+            const auto ta0 = std::chrono::steady_clock::now();
+            const cudaError_t ea = cudaMallocHost(&stage_[0], 2 * kChunk);
+            if (debug_)
+                std::fprintf(stderr, "[sskm] pinned staging %zu MB: %.2f ms\n", (2 * kChunk) >> 20,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta0).count());
+            if (ea != cudaSuccess) {  // no pinned memory: pageable copies
+                (void)cudaGetLastError();
+                stage_[0] = nullptr;
+                stage_failed_ = true;
+            } else {
+                stage_[1] = static_cast<char*>(stage_[0]) + kChunk;
+                for (int b = 0; b < 2; ++b) {
+                    CK(cudaEventCreateWithFlags(&stage_ev_[b], cudaEventDisableTiming));
+                    stage_used_[b] = false;
                 }
-                CK(cudaEventCreateWithFlags(&stage_ev_[b], cudaEventDisableTiming));
-                stage_used_[b] = false;
             }
+        }
         if (bytes < (size_t(8) << 20) || stage_failed_) {
             CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
             return;
@@ -186,7 +195,9 @@ public:
         for (int i = 0; off < bytes; ++i, off += kChunk) {
             const int b = i & 1;
             const size_t len = std::min(kChunk, bytes - off);
+            const auto tw0 = std::chrono::steady_clock::now();
             if (stage_used_[b]) CK(cudaEventSynchronize(stage_ev_[b]));
+            const auto tw1 = std::chrono::steady_clock::now();
             const char* s = static_cast<const char*>(src) + off;
             char* d = static_cast<char*>(stage_[b]);
             constexpr size_t kPiece = size_t(1) << 20;
@@ -196,9 +207,12 @@ public:
                 const size_t o = static_cast<size_t>(q) * kPiece;
                 std::memcpy(d + o, s + o, std::min(kPiece, len - o));
             }
+            const auto tw2 = std::chrono::steady_clock::now();
             CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage_[b], len, cudaMemcpyHostToDevice, stream_));
             CK(cudaEventRecord(stage_ev_[b], stream_));
             stage_used_[b] = true;
+            h2d_wait_ms_ += std::chrono::duration<double, std::milli>(tw1 - tw0).count();
+            h2d_copy_ms_ += std::chrono::duration<double, std::milli>(tw2 - tw1).count();
         }
     }
 
@@ -237,9 +251,9 @@ public:
         CK(cudaStreamSynchronize(stream_));
         const auto tu2 = std::chrono::steady_clock::now();
         if (debug_)
-            std::fprintf(stderr, "[sskm] upload: alloc %.2f ms, copy %.2f ms\n",
+            std::fprintf(stderr, "[sskm] upload: alloc %.2f ms, copy %.2f ms (staging: host copies %.2f ms, waits %.2f ms)\n",
                          std::chrono::duration<double, std::milli>(tu1 - tu0).count(),
-                         std::chrono::duration<double, std::milli>(tu2 - tu1).count());
+                         std::chrono::duration<double, std::milli>(tu2 - tu1).count(), h2d_copy_ms_, h2d_wait_ms_);
         reset_scalars();
         launch(validate_csr_kernel, grid_for(n, 256), 256, indptr_.p, idx_.p, val_.p, n, dims,
                                                                    &scal_.p->bad);
@@ -2499,6 +2513,7 @@ private:
     bool scalars_fresh_ = false;
     std::map<const void*, std::pair<int, int>> launch_cfg_;
     void* stage_[2] = {nullptr, nullptr};  // pinned upload staging (h2d)
+    double h2d_wait_ms_ = 0.0, h2d_copy_ms_ = 0.0;
     cudaEvent_t stage_ev_[2]{};
     bool stage_used_[2] = {false, false};
     bool stage_failed_ = false;  // pinned staging unavailable: pageable copies  // bound screen: (warps per block, blocks per SM)

@@ -1,5 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_bound.py tests/test_gpu_parity.py -x -q > gpurun_out/s4_lw_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/s4_lw_pytest.log
-for lib in scratch/lib_lw0.so scratch/lib_lw6.so paper_2108_00895_b200/libsskm_b200.so scratch/lib_lw12.so; do
+for lib in scratch/lib_mb5.so scratch/lib_mb3.so paper_2108_00895_b200/libsskm_b200.so; do
 for rep in 1 2; do
 SSKM_LIB=$PWD/$lib python scripts/probe_drift.py c1 33 --stats-only > gpurun_out/s4_lw.log 2>&1; echo "$lib rc=$?"
 python - <<PY
