@@ -357,7 +357,7 @@ public:
         Q_.alloc(2 * static_cast<size_t>(k_));
         part_.alloc(ceil_div(d_, kRowBlock) * k_);
         state_ = false;
-        have_cc_ = false;
+        have_cc_ = have_ids_ = false;
         cache_trusted_ = false;
         if (cfg_.mode != SSKM_MODE_BASELINE) cc_.alloc(static_cast<uint64_t>(d_) * ld_);
         obj_part_.alloc(kObjBlocks);
@@ -534,7 +534,7 @@ public:
         ub_valid_ = false;
         iteration_ = 0;
         dcum_rows_ = 0;
-        have_cc_ = false;
+        have_cc_ = have_ids_ = false;
         state_ = true;
         CK(cudaStreamSynchronize(stream_));
         if (seeds_out) std::memcpy(seeds_out, seeds.data(), k_ * 4);
@@ -957,7 +957,7 @@ public:
     void ncc_assign(sskm_iteration_stats* st) {
         CK(cudaEventRecord(ev_[2], stream_));
         snapshot_start();
-        ensure_cc();
+        ensure_cc(false);
         // the bound screen streams documents in index order (consecutive CSR rows:
         // measured 1.75 -> 1.40 ms per c1 screen against the cluster order the
         // tile scans prefer)
@@ -982,6 +982,7 @@ public:
             pull_scalars();
             n_rescan = hs_->n_rescan;
         } else if (n_chg_ > 0) {
+            ensure_cc(true);
             if (screen_enabled_) {
                 if (!screen_any(cc_.p, ld_cc_, n_chg_, chg_ids_.p, a_start_.p, order, n_, kInitNcc))
                     resolve<kInitNcc>(order, n_);
@@ -1166,7 +1167,7 @@ public:
         cmax_ = 1e-300;
         for (double q : nrm) cmax_ = std::max(cmax_, std::sqrt(q) * (1.0 + 1e-12));
         reset_sums();
-        have_cc_ = false;
+        have_cc_ = have_ids_ = false;
         cache_trusted_ = false;
         ub_valid_ = false;
         CK(cudaStreamSynchronize(stream_));
@@ -1175,7 +1176,7 @@ public:
     void set_unchanged(const uint8_t* flags) {
         need_state();
         CK(cudaMemcpyAsync(unchanged_.p, flags, k_, cudaMemcpyHostToDevice, stream_));
-        have_cc_ = false;
+        have_cc_ = have_ids_ = false;
         cache_trusted_ = false;
         CK(cudaStreamSynchronize(stream_));
     }
@@ -1398,7 +1399,7 @@ private:
         CK(cudaMemsetAsync(unchanged_.p, 0, k_, stream_));
         iteration_ = 0;
         dcum_rows_ = 0;
-        have_cc_ = false;
+        have_cc_ = have_ids_ = false;
         state_ = true;
     }
 
@@ -1534,7 +1535,7 @@ private:
         double max_drift;
         std::memcpy(&max_drift, &hs_->max_drift_bits, 8);
         advance_drift(max_drift);
-        have_cc_ = false;
+        have_cc_ = have_ids_ = false;
         std::memset(st, 0, sizeof(*st));
         st->iteration = iteration_;
         st->n_unchanged_centroids = n_unchanged_;
@@ -1571,20 +1572,27 @@ private:
         dcum_rows_ = iteration_ + 1;
     }
 
-    void ensure_cc() {
-        if (have_cc_) return;
-        launch(compact_ids_kernel, 1, 1024, unchanged_.p, k_, 0, chg_ids_.p, &scal_.p->n_chg);
-        CK_LAUNCH();
-        pull_scalars();
-        n_chg_ = hs_->n_chg;
-        ld_cc_ = std::max<uint64_t>(128, round_up(n_chg_, 128));
-        if (n_chg_ > 0) {
-            cc_.alloc(static_cast<uint64_t>(d_) * ld_);
-            launch(gather_cols_kernel, grid_for(static_cast<int64_t>(d_) * ld_cc_, 256), 256, 
-                ct_.p, ld_, d_, chg_ids_.p, n_chg_, cc_.p, ld_cc_);
+    // The changed-cluster ids and their count; with `cols`, also the compact
+    // copy of their columns (only the NCC passes over the changed list read it:
+    // the gather reads and writes up to all of Cᵀ, 0.45 ms on c1).
+    void ensure_cc(bool cols = true) {
+        if (!have_ids_) {
+            launch(compact_ids_kernel, 1, 1024, unchanged_.p, k_, 0, chg_ids_.p, &scal_.p->n_chg);
             CK_LAUNCH();
+            pull_scalars();
+            n_chg_ = hs_->n_chg;
+            ld_cc_ = std::max<uint64_t>(128, round_up(n_chg_, 128));
+            have_ids_ = true;
         }
-        have_cc_ = true;
+        if (cols && !have_cc_) {
+            if (n_chg_ > 0) {
+                cc_.alloc(static_cast<uint64_t>(d_) * ld_);
+                launch(gather_cols_kernel, grid_for(static_cast<int64_t>(d_) * ld_cc_, 256), 256, 
+                    ct_.p, ld_, d_, chg_ids_.p, n_chg_, cc_.p, ld_cc_);
+                CK_LAUNCH();
+            }
+            have_cc_ = true;
+        }
     }
 
     void snapshot_start() {
@@ -2465,7 +2473,7 @@ private:
     DevBuf<Scalars> scal_;
     Scalars* hs_ = nullptr;
 
-    bool corpus_ = false, state_ = false, have_cc_ = false;
+    bool corpus_ = false, state_ = false, have_cc_ = false, have_ids_ = false;
     int64_t n_ = 0, n_total_ = 0, doc_offset_ = 0, nnz_ = 0;
     uint32_t d_ = 0, k_ = 0, ld_ = 0;
     int K_ = 0;
@@ -2581,7 +2589,7 @@ private:
     double last_density_ = 0.0;
     double dense_above_ = 0.15;
     uint64_t dense_assigns_ = 0;
-    double ncc_full_frac_ = 0.25;
+    double ncc_full_frac_ = 0.0;  // SSKM_NCC_FULL_FRAC: NCC passes over the changed list only below this changed share (measured: the full screened scan with the drift bound is never slower)
     DevBuf<uint32_t> sa_, exact_;
     DevBuf<uint32_t> order_, keys32_;
     DevBuf<double> sims_, drift_, part_, obj_part_;

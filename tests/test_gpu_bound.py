@@ -75,6 +75,14 @@ def test_theta_and_screen_invariance(case, mode, monkeypatch):
         t, _ = trajectory(m, k, seeds, mode, iters)
         assert_same(ref, t, "tile passes")
         monkeypatch.delenv("SSKM_HASH")
+    if mode == "ncc":
+        # by default an exact-NCC step runs as the (bit-identical) full screened scan with the
+        # drift bound; the passes over the changed list (pass A, rescan) must give the same
+        for frac in ("2.0", "0.25"):
+            monkeypatch.setenv("SSKM_NCC_FULL_FRAC", frac)
+            t, _ = trajectory(m, k, seeds, mode, iters)
+            assert_same(ref, t, f"NCC changed-list passes (full frac {frac})")
+        monkeypatch.delenv("SSKM_NCC_FULL_FRAC")
     monkeypatch.setenv("SSKM_BOUND", "0")
     t, th = trajectory(m, k, seeds, mode, iters)
     assert_same(ref, t, "postings screen")
