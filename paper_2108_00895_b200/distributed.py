@@ -148,6 +148,8 @@ class Comm:
         return dist
 
     def all_reduce_i64(self, x: np.ndarray, op="sum") -> np.ndarray:
+        if self.world == 1:  # a collective over one rank is the identity: no device round trip
+            return np.ascontiguousarray(x, np.int64)
         import torch
         dist = self._d()
         t = torch.as_tensor(np.ascontiguousarray(x, np.int64)).to(self.dev)
@@ -155,6 +157,8 @@ class Comm:
         return t.cpu().numpy()
 
     def all_reduce_f64_max(self, x: float) -> float:
+        if self.world == 1:
+            return float(x)
         import torch
         dist = self._d()
         t = torch.tensor([x], dtype=torch.float64, device=self.dev)
@@ -162,6 +166,8 @@ class Comm:
         return float(t.item())
 
     def all_gather_f64(self, x: float) -> list:
+        if self.world == 1:
+            return [float(x)]
         import torch
         dist = self._d()
         t = torch.tensor([x], dtype=torch.float64, device=self.dev)
@@ -171,6 +177,8 @@ class Comm:
 
     def all_gather_var(self, t):
         """All-gather of a 1-D tensor of per-rank length; rank-ordered list."""
+        if self.world == 1:
+            return [t]
         import torch
         dist = self._d()
         src_dev = t.device
@@ -190,6 +198,8 @@ class Comm:
         """All-gather of several 1-D tensors of per-rank length: one gather of
         all the lengths, then one padded gather per tensor. Returns, per tensor,
         the rank-ordered list."""
+        if self.world == 1:
+            return [[t] for t in ts]
         import torch
         dist = self._d()
         src = [t.device for t in ts]
@@ -211,6 +221,8 @@ class Comm:
 
     def all_gather_f64_vec(self, x: np.ndarray) -> np.ndarray:
         """[world, len(x)] float64, rank-ordered rows."""
+        if self.world == 1:
+            return np.ascontiguousarray(x, np.float64).reshape(1, -1)
         import torch
         dist = self._d()
         t = torch.as_tensor(np.ascontiguousarray(x, np.float64)).to(self.dev)
@@ -219,6 +231,8 @@ class Comm:
         return out.view(self.world, -1).cpu().numpy()
 
     def all_gather_object(self, obj) -> list:
+        if self.world == 1:
+            return [obj]
         dist = self._d()
         out = [None] * self.world
         dist.all_gather_object(out, obj, group=self.group)
@@ -397,6 +411,8 @@ def init_process_group_from_env(backend: Optional[str] = None):
         return dist.get_rank(), dist.get_world_size()
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
+    if "RANK" not in os.environ:  # a single process outside torchrun (bench.py --distributed at N = 1)
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0"})
     backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
     dist.init_process_group(backend=backend)
     return dist.get_rank(), dist.get_world_size()
