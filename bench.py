@@ -55,22 +55,29 @@ def measured_peak_gbs():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.
+
+    The sampler process is started before the warm-up (forking it at the start
+    of the timed region delayed the first timed step's launches by 1-2 ms) and
+    polls every 20 ms; `begin()` / `end()` bracket the timed region and the
+    summary uses the samples that arrived inside it (plus one period after)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 20
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (arrival time, line)
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -80,36 +87,64 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def __exit__(self, *exc):
+    def begin(self):
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
+
+    def stop(self):
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(2.5 * self.PERIOD_MS / 1e3)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
 
+    # context-manager form: sampler started here, the whole block is the timed region
+    def __enter__(self):
+        if self.proc is None:
+            self.start()
+        self.begin()
+        return self
+
+    def __exit__(self, *exc):
+        self.end()
+        self.stop()
+
     def summary(self):
-        sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(name)
+
+        def collect(rows):
+            sm, mx, reasons = [], [], set()
+            for ln in rows:
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for name, v in zip(names, parts[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+            return sm, mx, reasons
+
+        inside = [ln for (t, ln) in self.lines
+                  if self.t0 is not None and self.t1 is not None and self.t0 <= t <= self.t1 + 2 * self.PERIOD_MS / 1e3]
+        sm, mx, reasons = collect(inside)
+        where = "timed region"
+        if not sm:  # a region shorter than the polling period: the nearest samples around it
+            sm, mx, reasons = collect([ln for _, ln in self.lines])
+            where = "around the timed region (shorter than the polling period)"
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sampled": where, "period_ms": self.PERIOD_MS}
 
 
 def ncu_traffic():
@@ -343,7 +378,8 @@ def run_ours(args):
     # every step between two events (slot s = start of step s): iteration 1 and
     # the warm-up steps are reported too; the timed region is slots W .. W+K
     all_stats = []
-    clk = ClockSampler(0)
+    clk = ClockSampler(0).start()  # running before the warm-up: nothing is forked inside the timed region
+    time.sleep(0.05)
     eng.synchronize()
     eng.timer_record(0)
     for s in range(W):
@@ -351,11 +387,13 @@ def run_ours(args):
         eng.timer_record(s + 1)
     eng.synchronize()
     l0 = eng.launch_count()
-    with clk:
-        for s in range(W, W + K):
-            all_stats.append(eng.step())
-            eng.timer_record(s + 1)
-        total_ms = eng.timer_elapsed(W, W + K)
+    clk.begin()
+    for s in range(W, W + K):
+        all_stats.append(eng.step())
+        eng.timer_record(s + 1)
+    total_ms = eng.timer_elapsed(W, W + K)
+    clk.end()
+    clk.stop()
     launches = eng.launch_count() - l0
     per_iter = [eng.timer_elapsed(s, s + 1) for s in range(W + K)]
     stats = all_stats[W:]

@@ -448,21 +448,23 @@ def bench_distributed(args, extras=None):
     comm = Comm(rank, world, torch.device("cuda", local))
     km = DistributedKMeans(gs, comm, data.n_docs, cfg.k, mode=args.mode)
     km.init_from_seeds(seeds)
+    # the clock sampler runs from before the warm-up (nothing is forked inside the timed region)
+    clock = extras["clock"](local).start() if "clock" in extras else None
     for _ in range(max(args.warmup, 3)):
         km.step()
     dist.barrier()
     torch.cuda.synchronize()
     gs.eng.synchronize()
-    clock = extras["clock"](local) if "clock" in extras else None
     if clock:
-        clock.__enter__()
+        clock.begin()
     gs.eng.timer_record(0)
     l0 = gs.eng.launch_count()
     stats = [km.step() for _ in range(args.steps)]
     gs.eng.timer_record(1)
     ms = gs.eng.timer_elapsed(0, 1)
     if clock:
-        clock.__exit__(None, None, None)
+        clock.end()
+        clock.stop()
     dist.barrier()
     ms_max = comm.all_reduce_f64_max(ms)
     launches = gs.eng.launch_count() - l0
