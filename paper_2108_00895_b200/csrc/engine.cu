@@ -90,6 +90,7 @@ public:
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_INDEX_ACCOUNTING")) index_accounting_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_REBUILD_LATE")) rebuild_late_ = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SSKM_SECOND_PASS")) second_pass_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SECOND_RATIO")) second_pass_ratio_ = static_cast<float>(std::atof(e));
@@ -733,7 +734,8 @@ public:
             ncc_assign(st);
             // engine.cpp:384-386: the reference builds its Lemma-1 index when
             // more than index_activation_threshold centroids changed
-            if (cfg_.mode == SSKM_MODE_NCC_INDEX && n_chg_ > cfg_.index_activation_threshold && cfg_.n_lambdas > 0)
+            if (cfg_.mode == SSKM_MODE_NCC_INDEX && index_accounting_ && n_chg_ > cfg_.index_activation_threshold &&
+                cfg_.n_lambdas > 0)
                 index_account(st);
         }
     }
@@ -2568,6 +2570,9 @@ private:
     double last_update_ms_ = 0.0;  // the last update's device time (θ tuning)
     uint64_t kpp_host_rounds_ = 0;  // k-means++ rounds the host had to replay (last seeding)
     bool skip_enabled_ = true;  // SSKM_SKIP=0: screen every document
+    // SSKM_INDEX_ACCOUNTING=0: `ncc+index` runs at the NCC step's speed and reports the NCC
+    // counters (index_active = 0) instead of replaying the reference's index for its counters
+    bool index_accounting_ = true;
     // second pass of the hash screens (bound_second_pass)
     bool second_pass_ = true;          // SSKM_SECOND_PASS=0: fallen-through documents go straight to the exact scan
     float second_pass_ratio_ = 0.5f;  // θ of the second lists relative to the first pass's (measured on c4)
