@@ -38,7 +38,12 @@ namespace sskm_b200 {
 #define SSKM_BOUND_MINB 4  // resident 256-thread blocks per SM the register budget is cut for
 #endif
 
-constexpr int kUbGroups = 32;            // drift bound: clusters grouped by id mod 32 (one group per lane)
+#ifndef SSKM_UB_GROUPS
+#define SSKM_UB_GROUPS 32
+#endif
+constexpr int kUbGroups = SSKM_UB_GROUPS;  // drift bound: clusters grouped by id mod kUbGroups (32 or 64)
+constexpr int kUbPerLane = kUbGroups / 32;  // groups lane, lane + 32, ... belong to a lane
+static_assert(kUbGroups == 32 || kUbGroups == 64, "the fold buffer holds at most 64 group maxima");
 constexpr unsigned short kHalfInf = 0x7C00u;
 constexpr float kFixScale = 0x1p30f;    // fixed-point products: q = rn(p · 2^30)
 constexpr double kFixUnit = 0x1p-30;
@@ -497,36 +502,50 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                 // pairs were accumulated). The fold buffer is free until the
                 // candidate dots.
                 const uint32_t s_gm = sb + SM::o_fold;
-                sm_st_u32(s_gm + 4u * lane, 0u);
+#pragma unroll
+                for (int q = 0; q < kUbPerLane; ++q) sm_st_u32(s_gm + 4u * (lane + kWarp * q), 0u);
                 __syncwarp();
+                constexpr uint32_t kGMask = static_cast<uint32_t>(kUbGroups - 1);
                 if (dense) {
-                    int m = 0;
-                    for (int c = lane; c < kSlots; c += kWarp) {
-                        const int v = static_cast<int>(sm_ld_u32(s_acc + 4u * c));
-                        if constexpr (HT > 0) {
-                            const uint32_t key = sm_ld_u32(s_key + 4u * c);
-                            if (key != 0 && v > 0)
-                                asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * ((key - 1u) & 31u)), "r"(v));
-                        } else {
-                            m = max(m, v);  // column c0 + c, c0 a multiple of 32: group = lane
+                    int m[kUbPerLane];
+#pragma unroll
+                    for (int q = 0; q < kUbPerLane; ++q) m[q] = 0;
+                    for (int c = lane; c < kSlots; c += kWarp * kUbPerLane) {
+#pragma unroll
+                        for (int q = 0; q < kUbPerLane; ++q) {
+                            const int cc = c + kWarp * q;  // kSlots is a multiple of 64
+                            const int v = static_cast<int>(sm_ld_u32(s_acc + 4u * cc));
+                            if constexpr (HT > 0) {
+                                const uint32_t key = sm_ld_u32(s_key + 4u * cc);
+                                if (key != 0 && v > 0)
+                                    asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * ((key - 1u) & kGMask)), "r"(v));
+                            } else {
+                                m[q] = max(m[q], v);  // column c0 + cc, c0 a multiple of 64: group = cc mod kUbGroups
+                            }
                         }
                     }
-                    if constexpr (HT == 0) sm_st_u32(s_gm + 4u * lane, static_cast<uint32_t>(m));
+                    if constexpr (HT == 0) {
+#pragma unroll
+                        for (int q = 0; q < kUbPerLane; ++q) sm_st_u32(s_gm + 4u * (lane + kWarp * q), static_cast<uint32_t>(m[q]));
+                    }
                 } else {
                     for (uint32_t kk = lane; kk < ntouch; kk += kWarp) {
                         const uint32_t jl = sm_ld_u16(s_tl + 2u * kk);
                         const int v = static_cast<int>(sm_ld_u32(s_acc + 4u * jl));
                         uint32_t col = p.c0 + jl;
                         if constexpr (HT > 0) col = sm_ld_u32(s_key + 4u * jl) - 1u;
-                        if (v > 0) asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * (col & 31u)), "r"(v));
+                        if (v > 0) asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * (col & kGMask)), "r"(v));
                     }
                 }
                 __syncwarp();
-                const int gmax = static_cast<int>(sm_ld_u32(s_gm + 4u * lane));
-                __half u = __float2half_ru(__double2float_ru(static_cast<double>(gmax) * kFixUnit + bx));
-                __half* ug = p.ub + static_cast<uint64_t>(i) * kUbGroups + lane;
-                if (!first) u = __hmax(u, *ug);
-                *ug = u;
+#pragma unroll
+                for (int q = 0; q < kUbPerLane; ++q) {
+                    const int gmax = static_cast<int>(sm_ld_u32(s_gm + 4u * (lane + kWarp * q)));
+                    __half u = __float2half_ru(__double2float_ru(static_cast<double>(gmax) * kFixUnit + bx));
+                    __half* ug = p.ub + static_cast<uint64_t>(i) * kUbGroups + lane + kWarp * q;
+                    if (!first) u = __hmax(u, *ug);
+                    *ug = u;
+                }
                 if (first && lane == 0) p.ub_it[i] = p.iter;
                 __syncwarp();  // the fold buffer goes back to the candidate dots
             }
@@ -694,16 +713,18 @@ constexpr int kSkipDocsPerBlock = 1024;
 // bounds). One block of 32 warps, warp g = group g.
 __global__ void __launch_bounds__(1024) group_drift_kernel(const double* __restrict__ drift_sq, uint32_t k, int ok,
                                                            double* __restrict__ dcum, uint32_t iter) {
-    const int lane = threadIdx.x & (kWarp - 1), g = threadIdx.x / kWarp;
-    double m = 0.0;
-    if (ok)
-        for (uint32_t j = g + kUbGroups * lane; j < k; j += kUbGroups * kWarp) m = fmax(m, drift_sq[j]);
+    const int lane = threadIdx.x & (kWarp - 1);
+    for (int g = threadIdx.x / kWarp; g < kUbGroups; g += blockDim.x / kWarp) {
+        double m = 0.0;
+        if (ok)
+            for (uint32_t j = g + kUbGroups * lane; j < k; j += kUbGroups * kWarp) m = fmax(m, drift_sq[j]);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
-    if (lane == 0) {
-        const double prev = iter > 0 ? dcum[static_cast<uint64_t>(iter - 1) * kUbGroups + g] : 0.0;
-        // a NaN or negative drift cannot be followed either: the host checks the maximum
-        dcum[static_cast<uint64_t>(iter) * kUbGroups + g] = prev + (ok && m > 0.0 ? sqrt(m) * (1.0 + 1e-9) : 0.0);
+        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
+        if (lane == 0) {
+            const double prev = iter > 0 ? dcum[static_cast<uint64_t>(iter - 1) * kUbGroups + g] : 0.0;
+            // a NaN or negative drift cannot be followed either: the host checks the maximum
+            dcum[static_cast<uint64_t>(iter) * kUbGroups + g] = prev + (ok && m > 0.0 ? sqrt(m) * (1.0 + 1e-9) : 0.0);
+        }
     }
 }
 
@@ -740,9 +761,10 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
         kp[q] = true;
         if (p.same[p.a[i]]) {
             const uint4* __restrict__ row = reinterpret_cast<const uint4*>(p.ub + static_cast<uint64_t>(i) * kUbGroups);
-            uint4 w[4];
+            constexpr int kV = kUbGroups / 8;  // 16-byte loads per document
+            uint4 w[kV];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) w[v] = row[v];
+            for (int v = 0; v < kV; ++v) w[v] = row[v];
             const uint32_t its = p.ub_it[i];
             const float x2 = p.xb[i].y;
             float bmax = 0.f;  // every rounding upward; +inf marks a withdrawn bound
@@ -754,7 +776,7 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
             if (its >= t_lo && its <= p.iter) {
                 const float* __restrict__ gr = G[its - t_lo];
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
+                for (int v = 0; v < kV; ++v) {
                     fold2(w[v].x, gr[8 * v + 0], gr[8 * v + 1]);
                     fold2(w[v].y, gr[8 * v + 2], gr[8 * v + 3]);
                     fold2(w[v].z, gr[8 * v + 4], gr[8 * v + 5]);
@@ -766,7 +788,7 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
                 const double* __restrict__ dt = p.dcum + static_cast<uint64_t>(its) * kUbGroups;
                 auto gg = [&](int g) { return __double2float_ru((dnow[g] - dt[g]) * (1.0 + 1e-9)); };
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
+                for (int v = 0; v < kV; ++v) {
                     fold2(w[v].x, gg(8 * v + 0), gg(8 * v + 1));
                     fold2(w[v].y, gg(8 * v + 2), gg(8 * v + 3));
                     fold2(w[v].z, gg(8 * v + 4), gg(8 * v + 5));
