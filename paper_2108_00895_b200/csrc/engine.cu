@@ -219,6 +219,7 @@ public:
 
     void upload(int64_t n, uint32_t dims, const int64_t* indptr, const int32_t* indices,
                 const float* values, int64_t doc_offset, int64_t n_total) {
+        counts_fresh_ = false;
         CK(cudaSetDevice(device_));
         // nothing of the previous corpus / configuration stays usable: the
         // buffers below are resized for the new corpus, and a failed validation
@@ -322,6 +323,7 @@ public:
     }
 
     void configure(const sskm_run_config& c) {
+        counts_fresh_ = false;
         CK(cudaSetDevice(device_));
         if (!corpus_) throw InvalidArgument("upload a corpus before configuring");
         validate(c, static_cast<uint64_t>(n_total_));
@@ -548,8 +550,14 @@ public:
         CK(cudaEventRecord(ev_[0], stream_));
         iteration_ += 1;
         repaired_.clear();
-        local_counts_device();
-        repair_empty_single();
+        if (counts_fresh_) {
+            // the last assign counted its clusters: none empty, every assignment in range
+            CK(cudaMemsetAsync(repaired_flag_.p, 0, k_, stream_));
+        } else {
+            local_counts_device();
+            repair_empty_single();
+        }
+        counts_fresh_ = false;
         // rows that moved since the sums were last brought up to date
         reset_scalars();
         launch(moved_kernel, grid_for(n_, 256), 256, a_.p, a_sum_.p, n_, moved_.p, &scal_.p->n_moved);
@@ -569,6 +577,7 @@ public:
     void update_apply(int64_t n_moved, const uint32_t* old_c, const uint32_t* new_c, const int64_t* row_ptr,
                       const int32_t* idx, const float* val, const uint32_t* repaired, uint32_t n_repaired,
                       sskm_iteration_stats* st) {
+        counts_fresh_ = false;
         need_state();
         CK(cudaEventRecord(ev_[0], stream_));
         iteration_ += 1;
@@ -616,6 +625,7 @@ public:
 
     // 1. local cluster sizes, copied to the host
     void mp_begin(unsigned long long* counts_host) {
+        counts_fresh_ = false;
         need_state();
         CK(cudaSetDevice(device_));
         CK(cudaEventRecord(ev_[0], stream_));
@@ -632,6 +642,7 @@ public:
     // pairs; the repaired clusters of every device), then the moved list
     void mp_moved(const std::vector<uint32_t>& local_moves, const std::vector<uint32_t>& repaired,
                   cudaEvent_t done) {
+        counts_fresh_ = false;
         CK(cudaSetDevice(device_));
         repaired_ = repaired;
         CK(cudaMemsetAsync(repaired_flag_.p, 0, k_, stream_));
@@ -1042,6 +1053,7 @@ public:
     }
 
     void set_state(const uint32_t* a, const double* sims, uint32_t iteration) {
+        counts_fresh_ = false;
         need_config();
         if (!state_) {
             reset_sums();
@@ -1199,6 +1211,7 @@ public:
     }
 
     void move_doc(int64_t global_doc, uint32_t cluster) {
+        counts_fresh_ = false;
         need_state();
         const int64_t i = global_doc - doc_offset_;
         if (i < 0 || i >= n_ || cluster >= k_) throw InvalidArgument("move_doc out of range");
@@ -1270,6 +1283,7 @@ public:
     // Multi-GPU seed init: centroid j = row j of a k-row CSR (host arrays) —
     // the seed documents gathered from whichever shard owns them.
     void init_from_rows(const int64_t* rptr, const int32_t* ridx, const float* rval) {
+        counts_fresh_ = false;
         need_config();
         hp_valid_ = false;
         const int64_t nnz = rptr[k_];
@@ -1410,14 +1424,18 @@ private:
         CK(cudaMemcpyAsync(a_sum_.p, a_.p, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
     }
 
-    void local_counts_device() {
-        CK(cudaMemsetAsync(counts_.p, 0, k_ * 8, stream_));
-        reset_scalars();
+    void launch_counts() {
         if (k_ <= kSmemBins)
             launch(counts_smem_kernel, static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(sms_, ceil_div(n_, 1024)))),
                    1024, a_.p, n_, k_, counts_.p, &scal_.p->bad);
         else
             launch(counts_kernel, grid_for(n_, 256), 256, a_.p, n_, k_, counts_.p, &scal_.p->bad);
+    }
+
+    void local_counts_device() {
+        CK(cudaMemsetAsync(counts_.p, 0, k_ * 8, stream_));
+        reset_scalars();
+        launch_counts();
         CK_LAUNCH();
     }
 
@@ -2424,12 +2442,20 @@ private:
         launch(finish_assign_kernel, kObjBlocks, 256, a_.p, a_start_.p, sims_.p, n_, obj_part_.p,
                                                               &scal_.p->reassigned);
         launch(sum_parts_kernel, 1, 256, obj_part_.p, kObjBlocks, &scal_.p->objective);
+        // the cluster sizes of the new assignment, so that the next update's
+        // empty-cluster check needs no round trip of its own (engine.cpp:154)
+        CK(cudaMemsetAsync(counts_.p, 0, k_ * 8, stream_));
+        CK(cudaMemsetAsync(&scal_.p->bad, 0, 4, stream_));
+        CK(cudaMemsetAsync(&scal_.p->n_empty, 0, 4, stream_));
+        launch_counts();
+        launch(count_empty_kernel, grid_for(k_, 256), 256, counts_.p, k_, &scal_.p->n_empty);
         CK_LAUNCH();
         CK(cudaEventRecord(ev_[3], stream_));
         pull_scalars();
         st->n_reassigned = hs_->reassigned;
         st->objective = hs_->objective;
         updates_since_assign_ = 0;
+        counts_fresh_ = hs_->n_empty == 0 && hs_->bad == 0;  // anything else takes the update's own check
     }
 
     void reset_scalars_keep_rescan() {
@@ -2521,6 +2547,7 @@ private:
     int post_warps_ = 8;
     bool cache_trusted_ = false;
     bool scalars_fresh_ = false;
+    bool counts_fresh_ = false;  // the last assign's cluster sizes: none empty, nothing since changed an assignment
     std::map<const void*, std::pair<int, int>> launch_cfg_;
     void* stage_[2] = {nullptr, nullptr};  // pinned upload staging (h2d)
     double h2d_wait_ms_ = 0.0, h2d_copy_ms_ = 0.0;
