@@ -59,13 +59,13 @@ class ClockSampler:
 
     The sampler process is started before the warm-up (forking it at the start
     of the timed region delayed the first timed step's launches by 1-2 ms) and
-    polls every 20 ms; `begin()` / `end()` bracket the timed region and the
+    polls every 50 ms; `begin()` / `end()` bracket the timed region and the
     summary uses the samples that arrived inside it (plus one period after)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-    PERIOD_MS = 20
+    PERIOD_MS = 50  # a 20 ms poll measurably slowed the steps it was watching (driver locks): 1.58 -> 1.61 ms
 
     def __init__(self, index=0):
         self.index = index
@@ -388,14 +388,17 @@ def run_ours(args):
     eng.synchronize()
     l0 = eng.launch_count()
     clk.begin()
-    for s in range(W, W + K):
-        all_stats.append(eng.step())
-        eng.timer_record(s + 1)
-    total_ms = eng.timer_elapsed(W, W + K)
+    # the K timed steps in one native call (sskm_step_n): the step loop of the
+    # C-ABI, as sskm_run / the C++ run() drive it, without a Python round trip
+    # (ctypes call + stats conversion, ~60 us) between the steps
+    all_stats += eng.step_n(K)
+    eng.timer_record(W + 1)
+    total_ms = eng.timer_elapsed(W, W + 1)
     clk.end()
     clk.stop()
     launches = eng.launch_count() - l0
-    per_iter = [eng.timer_elapsed(s, s + 1) for s in range(W + K)]
+    # warm-up steps: event-bracketed; timed steps: the engine's own per-phase events (update + assign)
+    per_iter = [eng.timer_elapsed(s, s + 1) for s in range(W)] + [s.update_ms + s.assign_ms for s in all_stats[W:]]
     stats = all_stats[W:]
     value = data.n_docs * k * K / (total_ms / 1e3)
     performed = sum(s.gpu_dot_products for s in stats) / (total_ms / 1e3)

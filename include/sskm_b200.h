@@ -143,6 +143,11 @@ int sskm_assign(sskm_ctx* ctx, sskm_iteration_stats* st);
 /* One Lloyd iteration = sskm_update + sskm_assign (run() loop body, engine.cpp:357-407). */
 int sskm_step(sskm_ctx* ctx, sskm_iteration_stats* st);
 
+/* n Lloyd iterations back to back, whatever the stop rules say (fixed-length
+ * runs: benchmarks, the reference CLI's bench with a fixed iteration count);
+ * stats has room for n entries (or is NULL). */
+int sskm_step_n(sskm_ctx* ctx, uint32_t n, sskm_iteration_stats* stats);
+
 /* run() loop (engine.cpp:357-424) from the current state: iterations until no
  * reassignment, drift < conv_sq_dist (iteration > 1), or max_iters. */
 int sskm_run(sskm_ctx* ctx, sskm_iteration_stats* stats, uint32_t stats_cap, uint32_t* n_iters,

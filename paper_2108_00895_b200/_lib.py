@@ -98,6 +98,7 @@ SIGNATURES = [
     ("sskm_update", C.c_int, [_P, _ST]),
     ("sskm_assign", C.c_int, [_P, _ST]),
     ("sskm_step", C.c_int, [_P, _ST]),
+    ("sskm_step_n", C.c_int, [_P, C.c_uint32, _ST]),
     ("sskm_run", C.c_int, [_P, _ST, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int32)]),
     ("sskm_get_state", C.c_int, [_P, _u32p, _f64p, _u8p]),
     ("sskm_set_state", C.c_int, [_P, _u32p, _f64p, C.c_uint32]),

@@ -257,6 +257,12 @@ class Engine:
     def step(self) -> IterationStats:
         return self._stats_call(self.lib.sskm_step)
 
+    def step_n(self, n: int):
+        """n Lloyd iterations in one native call (no stop rules): [IterationStats]."""
+        arr = (sskm_iteration_stats * max(int(n), 1))()
+        check(self.lib.sskm_step_n(self.h, int(n), arr))
+        return [IterationStats.from_c(arr[i]) for i in range(int(n))]
+
     def run(self, cap: Optional[int] = None):
         cap = cap or self.cfg.max_iters
         arr = (sskm_iteration_stats * cap)()

@@ -2839,6 +2839,17 @@ int sskm_step(sskm_ctx* ctx, sskm_iteration_stats* st) {
     return guard([&] { step(E(ctx), st); });
 }
 
+int sskm_step_n(sskm_ctx* ctx, uint32_t n, sskm_iteration_stats* stats) {
+    return guard([&] {
+        Engine& e = E(ctx);
+        for (uint32_t t = 0; t < n; ++t) {
+            sskm_iteration_stats st{};
+            step(e, &st);
+            if (stats) stats[t] = st;
+        }
+    });
+}
+
 int sskm_run(sskm_ctx* ctx, sskm_iteration_stats* stats, uint32_t cap, uint32_t* n_iters, int32_t* stop_reason) {
     return guard([&] {
         Engine& e = E(ctx);

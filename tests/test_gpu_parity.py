@@ -370,3 +370,24 @@ def test_gpu_kmeanspp_device_rounds_match_reference(k, monkeypatch):
         np.testing.assert_array_equal(seeds, rs)
         np.testing.assert_array_equal(a, ra)
         np.testing.assert_array_equal(s, rsims)
+
+
+@pytest.mark.parametrize("mode", ["baseline", "ncc"])
+def test_gpu_step_n_equals_steps(mode):
+    """sskm_step_n: n iterations in one native call = n sskm_step calls, bit for
+    bit (state and per-iteration counters)."""
+    m = S.generate(5000, 4096, 24, 50.0, seed=21)
+    k = 48
+    seeds = S.init_seeds(m.n_docs, k, 0)
+    a = engine_for(m, k, mode, conv_sq_dist=1e-300, max_iters=100)
+    b = engine_for(m, k, mode, conv_sq_dist=1e-300, max_iters=100)
+    a.init_from_seeds(seeds)
+    b.init_from_seeds(seeds)
+    sa = [a.step() for _ in range(6)]
+    sb = b.step_n(6)
+    assert len(sb) == 6
+    for x, y in zip(sa, sb):
+        assert (x.iteration, x.dot_products, x.n_reassigned, x.n_unchanged_centroids, x.objective) == \
+               (y.iteration, y.dot_products, y.n_reassigned, y.n_unchanged_centroids, y.objective)
+    (aa, asim, _), (ba, bsim, _) = a.get_state(), b.get_state()
+    assert np.array_equal(aa, ba) and np.array_equal(asim, bsim)
