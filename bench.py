@@ -253,11 +253,15 @@ def bound_screen_bytes(stats):
     the kernel's own counters: 8 B per high (cluster, value) pair, 16 B per
     document nonzero (idx, val and the two posting offsets of its term), 36 B per
     document visit (indptr pair, work-list id, running (arg, best) read and
-    written) and 4 B per centroid value gathered by a candidate's exact dot."""
+    written), 4 B per centroid value gathered by a candidate's exact dot or by an
+    own-cluster dot, and the 68 B the kernel writes per visited document for the
+    drift bound (32 fp16 group bounds + the iteration stamp)."""
     m = lambda f: statistics.mean(getattr(s, f) for s in stats)
     pairs, dnnz, visits, cnnz = m("bound_pairs"), m("bound_doc_nnz"), m("bound_visits"), m("bound_cand_nnz")
-    b = 8 * pairs + 16 * dnnz + 36 * visits + 4 * cnnz
-    return {"bytes": b, "high_pairs": pairs, "doc_nnz": dnnz, "visits": visits, "candidates": m("bound_candidates"),
+    onnz = m("bound_own_nnz")
+    ub = 68 * visits if any(s.skip_docs for s in stats) else 0  # the drift bound's outputs (full-scan passes)
+    b = 8 * pairs + 16 * dnnz + 36 * visits + 4 * cnnz + 4 * onnz + ub
+    return {"bytes": b, "own_dot_nnz": onnz, "high_pairs": pairs, "doc_nnz": dnnz, "visits": visits, "candidates": m("bound_candidates"),
             "own_dots": m("bound_own_dots"), "candidate_nnz": cnnz, "theta": m("bound_theta")}
 
 
@@ -277,8 +281,8 @@ def bound_roofline(stats, data):
            "launches_per_assign": statistics.mean(s.screen_launches for s in stats), "peak_source": peak_src,
            "dense_equivalent": {"bytes": bytes_dense, "gbs": bytes_dense / (screen_ms / 1e3) / 1e9 if screen_ms else 0,
                                 "note": "SURVEY 8d B_assign (4·Σ nnz_i·k): what a dense Ct scan would move"},
-           "note": "algorithmic bytes of the bound screen = 8·high pairs + 16·doc nnz read + 36·doc visits "
-                   "+ 4·candidate-dot nnz (DESIGN.md §3.1), over the kernel's CUDA-event time; "
+           "note": "algorithmic bytes of the bound screen = 8·high pairs + 16·doc nnz read + (36 + 68)·doc visits "
+                   "+ 4·(candidate-dot + own-dot) nnz (DESIGN.md §3.1), over the kernel's CUDA-event time; "
                    "traffic = ncu dram__bytes_read+write per launch of the same bench command "
                    "(profiles/r02_ncu_bound_summary.json)"}
     if traffic and summ:

@@ -96,7 +96,8 @@ typedef struct {
     uint64_t bound_visits;     /* documents visited by the bound-screen launches (all tiles) */
     uint64_t bound_own_dots;   /* exact own-cluster dots computed inside the screen (the rest were cached) */
     uint64_t skip_docs;        /* documents the drift bound kept in their cluster without a screen */
-    uint64_t reserved1, reserved2;
+    uint64_t bound_own_nnz;    /* document nonzeros of those own dots (= own-column weights gathered from C^T) */
+    uint64_t reserved2;
     double skip_ms;            /* CUDA-event time of the drift-bound pass */
 } sskm_iteration_stats;
 

@@ -69,7 +69,7 @@ class sskm_iteration_stats(C.Structure):
         ("bound_visits", C.c_uint64),
         ("bound_own_dots", C.c_uint64),
         ("skip_docs", C.c_uint64),
-        ("reserved1", C.c_uint64),
+        ("bound_own_nnz", C.c_uint64),
         ("reserved2", C.c_uint64),
         ("skip_ms", C.c_double),
     ]

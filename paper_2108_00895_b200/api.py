@@ -130,7 +130,7 @@ class IterationStats:
     bound_visits: int = 0
     bound_own_dots: int = 0
     skip_docs: int = 0
-    reserved1: int = 0
+    bound_own_nnz: int = 0
     reserved2: int = 0
     skip_ms: float = 0.0
 

@@ -93,6 +93,7 @@ struct BoundArgs {
     uint32_t iter;
     const unsigned long long* n_work_dev;  // work-list length on the device (overrides n_work)
     unsigned long long* n_hovf;      // documents whose hash table overflowed (HT > 0)
+    unsigned long long* n_own_nnz;   // nonzeros of the own dots (own-column weights gathered: roofline bytes)
 };
 
 // Per-warp shared memory of the bound screen (bytes). HT > 0: the
@@ -108,8 +109,8 @@ struct BoundSmem {
     static constexpr uint32_t o_fold = o_key + (HT > 0 ? HT * 4 : 0);  // double[32] fold buffer
     static constexpr uint32_t o_tl = o_fold + 32 * 8;      // u16[kCap] touched list
     static constexpr uint32_t o_cnt = o_tl + kCap * 2;     // u32 touched count
-    static constexpr uint32_t o_stats = o_cnt + 16;        // u32[8] per-warp statistics
-    static constexpr size_t per_warp = o_stats + 32;
+    static constexpr uint32_t o_stats = o_cnt + 16;        // u32[12] per-warp statistics (slot 7: the work range's end)
+    static constexpr size_t per_warp = o_stats + 48;
 };
 
 __device__ __forceinline__ uint32_t sm_ld_u32(uint32_t a) {
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     for (int c = lane; c < kSlots; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
     if constexpr (HT > 0)
         for (int c = lane; c < HT; c += kWarp) sm_st_u32(s_key + 4u * c, 0u);
-    if (lane < 7) sm_st_u32(s_st + 4u * lane, 0u);
+    if (lane < 12 && lane != 7) sm_st_u32(s_st + 4u * lane, 0u);
     __syncwarp();
     const uint2* __restrict__ pairs = p.pairs;
     const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
             if (need_dot) {
                 best = s_own;
                 stat(3, 1u);
+                stat(8, end - beg);
             }
             // no cluster without a high entry shared with x can exceed lb
             // (the tile's low maxima bound the clusters of this tile only)
@@ -661,6 +663,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         atomicAdd(p.n_cand, static_cast<unsigned long long>(sm_ld_u32(s_st + 16)));
         atomicAdd(p.n_cand_nnz, static_cast<unsigned long long>(sm_ld_u32(s_st + 20)));
         if (HT > 0 && p.n_hovf) atomicAdd(p.n_hovf, static_cast<unsigned long long>(sm_ld_u32(s_st + 24)));
+        if (p.n_own_nnz) atomicAdd(p.n_own_nnz, static_cast<unsigned long long>(sm_ld_u32(s_st + 32)));
     }
 #undef w1
 }

@@ -1619,6 +1619,7 @@ private:
         screen_ms_ = 0.0;
         screen_launches_ = 0;
         bstat_docs_ = bstat_pairs_ = bstat_cand_ = bstat_doc_nnz_ = bstat_cand_nnz_ = bstat_visits_ = bstat_own_ = 0;
+        bstat_own_nnz_ = 0;
         bstat_theta_ = 0.0;
         dots_ = 0;
         skip_docs_ = 0;
@@ -1784,6 +1785,7 @@ private:
         p.n_doc_nnz = bctr_.p + 4;
         p.n_cand_nnz = bctr_.p + 5;
         p.n_hovf = bctr_.p + 6;
+        p.n_own_nnz = bctr_.p + 7;
         // drift bound: single-tile full-scan passes over every document refresh
         // the per-document bounds; with valid bounds, a pre-pass first keeps
         // the documents that provably keep their cluster (skip_kernel)
@@ -1884,7 +1886,7 @@ private:
                    sims_start_.p, sims_.p, unchanged_.p, rescan_.p, &scal_.p->n_rescan);
         // θ for the next assign: keep the exact-scan share small and the
         // candidate dots near one per document (θ never changes a result)
-        unsigned long long ctr[7] = {0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0}, sk[4] = {0, 0, 0, 0};
+        unsigned long long ctr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0}, sk[4] = {0, 0, 0, 0};
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hp, hpctr_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
@@ -1919,6 +1921,7 @@ private:
         bstat_cand_ += ctr[0];
         bstat_visits_ += ctr[2];
         bstat_own_ += ctr[3];
+        bstat_own_nnz_ += ctr[7];
         bstat_doc_nnz_ += ctr[4];
         bstat_cand_nnz_ += ctr[5];
         bstat_theta_ = static_cast<double>(thr);
@@ -2027,7 +2030,7 @@ private:
         bound_launch_k(bound_screen_kernel<2048, kInitFull, HT2>, BoundSmem<2048, HT2>::per_warp, p);
         CK(cudaEventRecord(ev_[7], stream_));
         screen_launches_ += 1;
-        unsigned long long ctr[7] = {0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0};
+        unsigned long long ctr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0};
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hp, hpctr2_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
@@ -2044,6 +2047,7 @@ private:
         bstat_cand_ += ctr[0];
         bstat_visits_ += ctr[2];
         bstat_own_ += ctr[3];
+        bstat_own_nnz_ += ctr[7];
         bstat_doc_nnz_ += ctr[4];
         bstat_cand_nnz_ += ctr[5];
         if (debug_)
@@ -2480,6 +2484,7 @@ private:
         st->bound_theta = bstat_theta_;
         st->bound_visits = bstat_visits_;
         st->bound_own_dots = bstat_own_;
+        st->bound_own_nnz = bstat_own_nnz_;
         st->skip_docs = skip_docs_;
         st->second_pass_docs = static_cast<uint32_t>(std::min<uint64_t>(second_docs_, 0xFFFFFFFFull));
         st->skip_ms = skip_ms_;
@@ -2570,6 +2575,7 @@ private:
     // per-assign bound-screen totals (stats)
     uint64_t bstat_docs_ = 0, bstat_pairs_ = 0, bstat_cand_ = 0, bstat_doc_nnz_ = 0, bstat_cand_nnz_ = 0,
              bstat_visits_ = 0, bstat_own_ = 0;
+    uint64_t bstat_own_nnz_ = 0;
     uint32_t updates_since_assign_ = 0;  // updates since the last assign (the same_ flags' validity)
     double bstat_theta_ = 0.0;
     uint64_t dots_ = 0;
@@ -2768,6 +2774,7 @@ void step(Engine& e, sskm_iteration_stats* st) {
     st->bound_theta = a.bound_theta;
     st->bound_visits = a.bound_visits;
     st->bound_own_dots = a.bound_own_dots;
+    st->bound_own_nnz = a.bound_own_nnz;
     st->skip_docs = a.skip_docs;
     st->second_pass_docs = a.second_pass_docs;
     st->skip_ms = a.skip_ms;

@@ -38,7 +38,7 @@ for it in range(1, iters + 1):
                           "pairs": st.bound_pairs, "doc_nnz": st.bound_doc_nnz, "visits": st.bound_visits,
                           "cand": st.bound_candidates, "cand_nnz": st.bound_cand_nnz,
                           "alg_bytes": 8 * st.bound_pairs + 16 * st.bound_doc_nnz + 36 * st.bound_visits
-                                       + 4 * st.bound_cand_nnz}), flush=True)
+                                       + 4 * st.bound_cand_nnz + 4 * st.bound_own_nnz + 68 * st.bound_visits}), flush=True)
         continue
     ct = eng.get_centroids()
     d = np.sqrt(((ct.astype(np.float64) - prev) ** 2).sum(0))
