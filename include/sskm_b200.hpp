@@ -177,6 +177,12 @@ public:
     IterationStats update() { return call(sskm_update); }
     IterationStats assign() { return call(sskm_assign); }
     IterationStats step() { return call(sskm_step); }
+    /// n iterations back to back, no stop rules (fixed-length runs).
+    std::vector<IterationStats> step_n(std::uint32_t n) {
+        std::vector<IterationStats> st(n);
+        check(sskm_step_n(ctx_, n, st.data()));
+        return st;
+    }
     void state(std::vector<std::uint32_t>& a, std::vector<double>& sims, std::vector<std::uint8_t>& unchanged) {
         a.resize(n_);
         sims.resize(n_);
