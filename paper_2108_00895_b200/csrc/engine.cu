@@ -91,6 +91,7 @@ public:
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_INDEX_ACCOUNTING")) index_accounting_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_WG_ROWS")) wg_rows_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_REBUILD_LATE")) rebuild_late_ = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("SSKM_SECOND_PASS")) second_pass_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SECOND_RATIO")) second_pass_ratio_ = static_cast<float>(std::atof(e));
@@ -1532,9 +1533,16 @@ private:
         // partials reduced in a fixed order, then the NCC flags
         const uint32_t n_rb = static_cast<uint32_t>(ceil_div(d_, kRowBlock));
         const uint32_t n_groups = static_cast<uint32_t>(ceil_div(k_, 32));
-        launch(write_groups_kernel, dim3(static_cast<unsigned>(ceil_div(n_groups, 4)), n_rb), 128, S_.p, ct_.p,
-               (uint64_t)ld_, d_, k_, touched_.p, Q_.p, part_.p, &scal_.p->zero_flag, nz_.p, hptr_.p, pairs_.p,
-               keep_lists_ && hp_valid_ ? hp_theta_ : 0.f, &scal_.p->hp_ovf);
+        const dim3 wg_grid(static_cast<unsigned>(ceil_div(n_groups, 4)), n_rb);
+        const float wg_thr = keep_lists_ && hp_valid_ ? hp_theta_ : 0.f;
+#define SSKM_WG_LAUNCH(R)                                                                                         \
+    launch(write_groups_kernel<R>, wg_grid, 128, S_.p, ct_.p, (uint64_t)ld_, d_, k_, touched_.p, Q_.p, part_.p, \
+           &scal_.p->zero_flag, nz_.p, hptr_.p, pairs_.p, wg_thr, &scal_.p->hp_ovf)
+        if (wg_rows_ == 4)
+            SSKM_WG_LAUNCH(4);
+        else
+            SSKM_WG_LAUNCH(2);
+#undef SSKM_WG_LAUNCH
         launch(reduce_groups_kernel, static_cast<unsigned>(ceil_div(k_, 32)), 1024, part_.p, n_rb, k_, touched_.p,
                drift_.p, &scal_.p->n_rec);
         launch(flags_kernel, grid_for(k_, 256), 256, k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon,
@@ -2588,6 +2596,7 @@ private:
     bool ub_valid_ = false;     // every document's bound is valid for the current assignments
     // high postings kept across passes (single cluster tile over Cᵀ)
     static constexpr uint32_t kRebuildEvery = 4;
+    int wg_rows_ = 2;  // SSKM_WG_ROWS: marked rows per round of the column rewrite (2, or 4 for A/B runs)
     uint32_t rebuild_late_ = 16;  // SSKM_REBUILD_LATE: the period once few columns change per update
     // The kept lists are rebuilt for fresh, tight L_t (maintenance only ever
     // raises them) and to re-tune θ: every 4 assigns while the centroids still
