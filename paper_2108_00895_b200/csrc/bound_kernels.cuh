@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(256) skip_kernel(SkipArgs p) {
 // rewrite then maintains the lists in place from one iteration to the next
 // (hipost_maintain); a row without room (w = 0) raises the rebuild flag on its
 // first append.
-__global__ void __launch_bounds__(256) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
+__global__ void __launch_bounds__(256, 8) hipost_build_kernel(const float* __restrict__ M, uint64_t ld, uint32_t d,
                                                            uint32_t c0, uint32_t kt, float thr,
                                                            uint4* __restrict__ hptr, uint2* __restrict__ pairs,
                                                            unsigned long long cap, unsigned long long* total,
