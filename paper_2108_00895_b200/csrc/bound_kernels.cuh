@@ -105,8 +105,10 @@ struct BoundSmem {
     static constexpr int kCap = 256;  // touched slots tracked before a dense sweep of the table
     static constexpr int kSlots = HT > 0 ? HT : KT;
     static constexpr uint32_t o_acc = 0;                          // int32[kSlots] fixed-point accumulators
-    static constexpr uint32_t o_key = o_acc + kSlots * 4;         // u32[HT] hash keys: column + 1 (0 = empty)
-    static constexpr uint32_t o_fold = o_key + (HT > 0 ? HT * 4 : 0);  // double[32] fold buffer
+    // u16[HT] hash keys: column + 1 (0 = empty): hash passes need k <= 65,534. (16-bit keys
+    // bring the 1024-slot tables to 6 KB per warp: 32 resident warps per SM instead of 24.)
+    static constexpr uint32_t o_key = o_acc + kSlots * 4;
+    static constexpr uint32_t o_fold = o_key + (HT > 0 ? HT * 2 : 0);  // double[32] fold buffer
     static constexpr uint32_t o_tl = o_fold + 32 * 8;      // u16[kCap] touched list
     static constexpr uint32_t o_cnt = o_tl + kCap * 2;     // u32 touched count
     static constexpr uint32_t o_stats = o_cnt + 16;        // u32[12] per-warp statistics (slot 7: the work range's end)
@@ -132,9 +134,11 @@ __device__ __forceinline__ int sm_atom_add(uint32_t a, int v) {
     asm volatile("atom.shared.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
     return old;
 }
-__device__ __forceinline__ uint32_t sm_atom_cas(uint32_t a, uint32_t cmp, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v));
+__device__ __forceinline__ uint32_t sm_atom_cas16(uint32_t a, uint32_t cmp, uint32_t v) {
+    uint16_t old;
+    asm volatile("atom.shared.cas.b16 %0, [%1], %2, %3;"
+                 : "=h"(old)
+                 : "r"(a), "h"(static_cast<uint16_t>(cmp)), "h"(static_cast<uint16_t>(v)));
     return old;
 }
 
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
     const uint32_t s_key = sb + SM::o_key;
     for (int c = lane; c < kSlots; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
     if constexpr (HT > 0)
-        for (int c = lane; c < HT; c += kWarp) sm_st_u32(s_key + 4u * c, 0u);
+        for (int c = lane; c < HT / 2; c += kWarp) sm_st_u32(s_key + 4u * c, 0u);  // two keys per word
     if (lane < 12 && lane != 7) sm_st_u32(s_st + 4u * lane, 0u);
     __syncwarp();
     const uint2* __restrict__ pairs = p.pairs;
@@ -382,9 +386,9 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                                 uint32_t slot = kNone;
 #pragma unroll 1
                                 for (int probe = 0; probe < 64; ++probe) {
-                                    uint32_t key = sm_ld_u32(s_key + 4u * h);
+                                    uint32_t key = sm_ld_u16(s_key + 2u * h);
                                     if (key == 0) {
-                                        key = sm_atom_cas(s_key + 4u * h, 0u, pr.x + 1u);
+                                        key = sm_atom_cas16(s_key + 2u * h, 0u, pr.x + 1u);
                                         if (key == 0) {
                                             const uint32_t pos = static_cast<uint32_t>(sm_atom_add(s_cnt, 1));
                                             if (pos < static_cast<uint32_t>(kCap)) sm_st_u16(s_tl + 2u * pos, h);
@@ -518,7 +522,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                             const int cc = c + kWarp * q;  // kSlots is a multiple of 64
                             const int v = static_cast<int>(sm_ld_u32(s_acc + 4u * cc));
                             if constexpr (HT > 0) {
-                                const uint32_t key = sm_ld_u32(s_key + 4u * cc);
+                                const uint32_t key = sm_ld_u16(s_key + 2u * cc);
                                 if (key != 0 && v > 0)
                                     asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * ((key - 1u) & kGMask)), "r"(v));
                             } else {
@@ -535,7 +539,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                         const uint32_t jl = sm_ld_u16(s_tl + 2u * kk);
                         const int v = static_cast<int>(sm_ld_u32(s_acc + 4u * jl));
                         uint32_t col = p.c0 + jl;
-                        if constexpr (HT > 0) col = sm_ld_u32(s_key + 4u * jl) - 1u;
+                        if constexpr (HT > 0) col = sm_ld_u16(s_key + 2u * jl) - 1u;
                         if (v > 0) asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_gm + 4u * (col & kGMask)), "r"(v));
                     }
                 }
@@ -593,7 +597,7 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
                     uint32_t col = p.c0 + jl;
                     bool used = true;
                     if constexpr (HT > 0) {
-                        const uint32_t key = sm_ld_u32(s_key + 4u * jl);
+                        const uint32_t key = sm_ld_u16(s_key + 2u * jl);
                         used = key != 0;
                         col = key - 1u;
                     }
@@ -645,12 +649,12 @@ __global__ void __launch_bounds__(256, SSKM_BOUND_MINB) bound_screen_kernel(Boun
         if (dense) {
             for (int c = lane; c < kSlots; c += kWarp) sm_st_u32(s_acc + 4u * c, 0u);
             if constexpr (HT > 0)
-                for (int c = lane; c < HT; c += kWarp) sm_st_u32(s_key + 4u * c, 0u);
+                for (int c = lane; c < HT / 2; c += kWarp) sm_st_u32(s_key + 4u * c, 0u);
         } else {
             for (uint32_t kk = lane; kk < ntouch; kk += kWarp) {
                 const uint32_t sl = sm_ld_u16(s_tl + 2u * kk);
                 sm_st_u32(s_acc + 4u * sl, 0u);
-                if constexpr (HT > 0) sm_st_u32(s_key + 4u * sl, 0u);
+                if constexpr (HT > 0) sm_st_u16(s_key + 2u * sl, 0u);
             }
         }
         __syncwarp();

@@ -1745,7 +1745,7 @@ private:
         CK(cudaMemsetAsync(bctr_.p, 0, 8 * sizeof(unsigned long long), stream_));
         // more than one 2048-column tile: one pass with hash-table accumulators
         // over every column (SSKM_HASH=0: a pass per tile)
-        const bool hash = ncols > 2048 && hash_enabled_;
+        const bool hash = ncols > 2048 && ncols <= 65534 && hash_enabled_;  // 16-bit table keys (column + 1)
         const uint32_t KT = hash ? ncols : (ncols <= 1024 ? 1024 : 2048);
         // single-pass lists over Cᵀ are kept from pass to pass, maintained in
         // place by the column rewrite; rebuilt (and θ re-tuned) every
