@@ -90,6 +90,7 @@ public:
         if (const char* e = std::getenv("SSKM_FUSE_RESOLVE")) fuse_resolve_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_BOUND")) bound_enabled_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_SKIP")) skip_enabled_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SSKM_SPECULATE")) speculate_ok_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_INDEX_ACCOUNTING")) index_accounting_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SSKM_WG_ROWS")) wg_rows_ = std::atoi(e);
         if (const char* e = std::getenv("SSKM_REBUILD_LATE")) rebuild_late_ = std::max(1, std::atoi(e));
@@ -948,15 +949,20 @@ public:
         CK(cudaEventRecord(ev_[4], stream_));
         uint64_t n_exact = 0;
         if (screen_enabled_) {
+            // (the closing kernels ride along with the screen when the last full
+            // scan left no document for the exact scan: bound_assign)
+            speculate_finish_ = speculate_ok_ && last_full_n_exact_ == 0 && order == nullptr;
             if (!screen_any(ct_.p, ld_, k_, nullptr, nullptr, order, n_, kInitFull)) resolve<kInitFull>(order, n_);
+            speculate_finish_ = false;
             pull_scalars_unless_fresh();
             n_exact = hs_->n_exact;
+            last_full_n_exact_ = n_exact;
             if (n_exact > 0) scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, exact_.p, static_cast<int64_t>(n_exact));
         } else {
             scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, order, n_);
         }
         if (!bound_active()) ub_valid_ = false;
-        CK(cudaEventRecord(ev_[5], stream_));
+        if (!finish_speculated_) CK(cudaEventRecord(ev_[5], stream_));
         finish_assign(st);
         cache_trusted_ = true;
         st->n_unchanged_centroids = iteration_ <= 1 ? 0 : n_unchanged_;
@@ -1894,6 +1900,17 @@ private:
                    sims_start_.p, sims_.p, unchanged_.p, rescan_.p, &scal_.p->n_rescan);
         // θ for the next assign: keep the exact-scan share small and the
         // candidate dots near one per document (θ never changes a result)
+        // A full-scan pass that left nothing for the exact scan last time: the
+        // assign's closing kernels go out now, ahead of the counters' round trip,
+        // so the step has one host synchronisation fewer. If this pass does leave
+        // documents (the counters say so), the closing kernels simply run again
+        // after the exact scan.
+        const bool speculate = speculate_finish_ && init == kInitFull && full_cover && !hash;
+        if (speculate) {
+            CK(cudaEventRecord(ev_[5], stream_));
+            finish_assign_launch();
+            CK(cudaEventRecord(ev_[3], stream_));
+        }
         unsigned long long ctr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0}, sk[4] = {0, 0, 0, 0};
         CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
         CK(cudaMemcpyAsync(hp, hpctr_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
@@ -1913,6 +1930,7 @@ private:
         if (!reuse) last_hp_overflow_ = hp[1] != 0;
         if (last_hp_overflow_) hp_valid_ = false;
         const uint64_t n_fb = hs_->n_exact;
+        finish_speculated_ = speculate && n_fb == 0;
         {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, ev_[6], ev_[7]));
@@ -2449,21 +2467,29 @@ private:
         launch_tile_u<INIT, 16>(v, grid, p);
     }
 
-    void finish_assign(sskm_iteration_stats* st) {
+    // The assign's closing kernels: reassignment count and objective, then the
+    // cluster sizes of the new assignment, so that the next update's empty-
+    // cluster check needs no round trip of its own (engine.cpp:154).
+    void finish_assign_launch() {
         reset_scalars_keep_rescan();
         launch(finish_assign_kernel, kObjBlocks, 256, a_.p, a_start_.p, sims_.p, n_, obj_part_.p,
                                                               &scal_.p->reassigned);
         launch(sum_parts_kernel, 1, 256, obj_part_.p, kObjBlocks, &scal_.p->objective);
-        // the cluster sizes of the new assignment, so that the next update's
-        // empty-cluster check needs no round trip of its own (engine.cpp:154)
         CK(cudaMemsetAsync(counts_.p, 0, k_ * 8, stream_));
         CK(cudaMemsetAsync(&scal_.p->bad, 0, 4, stream_));
         CK(cudaMemsetAsync(&scal_.p->n_empty, 0, 4, stream_));
         launch_counts();
         launch(count_empty_kernel, grid_for(k_, 256), 256, counts_.p, k_, &scal_.p->n_empty);
         CK_LAUNCH();
-        CK(cudaEventRecord(ev_[3], stream_));
-        pull_scalars();
+    }
+
+    void finish_assign(sskm_iteration_stats* st) {
+        if (!finish_speculated_) {
+            finish_assign_launch();
+            CK(cudaEventRecord(ev_[3], stream_));
+            pull_scalars();
+        }
+        finish_speculated_ = false;
         st->n_reassigned = hs_->reassigned;
         st->objective = hs_->objective;
         updates_since_assign_ = 0;
@@ -2560,6 +2586,9 @@ private:
     int post_warps_ = 8;
     bool cache_trusted_ = false;
     bool scalars_fresh_ = false;
+    // the assign's closing kernels launched ahead of the screen's counters (bound_assign)
+    bool speculate_ok_ = true, speculate_finish_ = false, finish_speculated_ = false;
+    uint64_t last_full_n_exact_ = 1;
     bool counts_fresh_ = false;  // the last assign's cluster sizes: none empty, nothing since changed an assignment
     std::map<const void*, std::pair<int, int>> launch_cfg_;
     void* stage_[2] = {nullptr, nullptr};  // pinned upload staging (h2d)
