@@ -212,3 +212,22 @@ def test_replay_repair_needs_longer_lists_when_truncated():
     assert D.replay_repair(np.array([0, 3, 1]), [cand0, cand1], [10, 2], 1) is None
     moves = D.replay_repair(counts, [cand0, cand1], [1, 2], 1)
     assert moves == [(5, 2, 0)]
+
+
+def test_single_rank_collectives_are_identities():
+    """A collective over one rank is the identity: Comm(world=1) answers without
+    touching torch.distributed (no process group exists here) and in the shapes
+    the multi-rank paths return."""
+    c = D.Comm(0, 1, torch.device("cpu"))
+    x = np.arange(5, dtype=np.int64)
+    assert np.array_equal(c.all_reduce_i64(x), x)
+    assert c.all_reduce_f64_max(2.5) == 2.5
+    assert c.all_gather_f64(1.25) == [1.25]
+    t = torch.arange(7, dtype=torch.int32)
+    (g,) = c.all_gather_var(t)
+    assert torch.equal(g, t)
+    a, b = c.all_gather_var_multi([t, t.float()])
+    assert len(a) == 1 and torch.equal(a[0], t) and torch.equal(b[0], t.float())
+    v = c.all_gather_f64_vec(np.array([1.0, 2.0]))
+    assert v.shape == (1, 2) and v[0, 1] == 2.0
+    assert c.all_gather_object({"k": 1}) == [{"k": 1}]
