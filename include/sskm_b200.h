@@ -81,7 +81,7 @@ typedef struct {
     uint64_t n_exact;         /* documents the screen handed to the exact fp64 tile scan */
     double update_ms;         /* device time of compute_centroids + detect_unchanged */
     double assign_ms;         /* device time of the assignment step */
-    double assign_kernel_ms;  /* device time of the assign kernels (screen, resolve, exact) */
+    double assign_kernel_ms;  /* = assign_ms (a separate event pair was dropped: two launches on the host's path) */
     double screen_ms;         /* device time of the screen kernel launches only (bound or postings screen) */
     uint32_t screen_launches; /* screen launches in this assign (one per cluster tile) */
     uint32_t second_pass_docs; /* hash screens: documents the first pass left that a second pass (lower theta, larger tables) screened */

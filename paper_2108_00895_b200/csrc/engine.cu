@@ -55,23 +55,63 @@ struct Scalars {
     double objective;
 };
 
+// Scalars and the screens' counters, contiguous (Engine::pull_block).
+struct CounterBlock {
+    Scalars s;
+    unsigned long long bctr[8];  // bound screen counters
+    unsigned long long sk[4];    // drift-bound pass: work-list length, documents kept (zeroed with bctr)
+    unsigned long long hp[2];    // high-postings build: pairs reserved, lists dropped (kept across passes)
+};
+
+static_assert(offsetof(CounterBlock, sk) == offsetof(CounterBlock, bctr) + 8 * sizeof(unsigned long long),
+              "the screen's and the drift-bound pass's counters are zeroed by one memset");
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    bool owned = true;
     void alloc(size_t count) {
         if (count <= n && p) return;
         free();
         CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
         n = count;
+        owned = true;
+    }
+    // a fixed-size window of another allocation (never grown, not freed here)
+    void view(T* ptr, size_t count) {
+        free();
+        p = ptr;
+        n = count;
+        owned = false;
     }
     void free() {
-        if (p) cudaFree(p);
+        if (p && owned) cudaFree(p);
         p = nullptr;
         n = 0;
+        owned = true;
     }
     ~DevBuf() { free(); }
 };
+
+__global__ void zero_update_kernel(uint8_t* repaired_flag, uint32_t k, Scalars* sc) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < k) repaired_flag[j] = 0;
+    if (j == 0) *sc = Scalars{};
+}
+
+// Zeroes what the assign's closing kernels accumulate into: the cluster sizes
+// and the reassignment count, objective, range check and empty count.
+__global__ void zero_closing_kernel(unsigned long long* counts, uint32_t k, Scalars* sc) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < k) counts[j] = 0ull;
+    if (j == 0) {
+        sc->reassigned = 0ull;
+        sc->objective = 0.0;
+        sc->bad = 0u;
+        sc->n_empty = 0u;
+    }
+}
 
 class Engine {
 public:
@@ -118,8 +158,16 @@ public:
         CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
         for (auto& e : ev_) CK(cudaEventCreate(&e));
         for (auto& e : user_ev_) CK(cudaEventCreate(&e));
-        scal_.alloc(1);
-        CK(cudaMallocHost(&hs_, sizeof(Scalars)));
+        // the step's scalars and the screens' counters in one device block with
+        // one pinned host mirror: one copy brings them all back
+        ctr_block_.alloc(1);
+        CK(cudaMemsetAsync(ctr_block_.p, 0, sizeof(CounterBlock), stream_));
+        scal_.view(&ctr_block_.p->s, 1);
+        bctr_.view(ctr_block_.p->bctr, 8);
+        hpctr_.view(ctr_block_.p->hp, 2);
+        skip_ctr_.view(ctr_block_.p->sk, 4);
+        CK(cudaMallocHost(&hblock_, sizeof(CounterBlock)));
+        hs_ = &hblock_->s;
         // the screen keeps hot Cᵀ rows in L1: give L1 the whole carveout
         for (auto k : {screen_tile_kernel<1, 16>, screen_tile_kernel<2, 16>, screen_tile_kernel<4, 16>})
             CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
@@ -134,7 +182,7 @@ public:
             if (stage_ev_[b]) cudaEventDestroy(stage_ev_[b]);
         for (auto& e : user_ev_) cudaEventDestroy(e);
         cudaStreamDestroy(stream_);
-        if (hs_) cudaFreeHost(hs_);
+        if (hblock_) cudaFreeHost(hblock_);
     }
 
     // Every kernel goes through here: one place to count launches (bench's
@@ -553,15 +601,16 @@ public:
         iteration_ += 1;
         repaired_.clear();
         if (counts_fresh_) {
-            // the last assign counted its clusters: none empty, every assignment in range
-            CK(cudaMemsetAsync(repaired_flag_.p, 0, k_, stream_));
+            // the last assign counted its clusters: none empty, every assignment in
+            // range; one kernel clears the repaired flags and the step's scalars
+            launch(zero_update_kernel, grid_for(k_, 256), 256, repaired_flag_.p, k_, scal_.p);
         } else {
             local_counts_device();
             repair_empty_single();
+            reset_scalars();
         }
         counts_fresh_ = false;
         // rows that moved since the sums were last brought up to date
-        reset_scalars();
         launch(moved_kernel, grid_for(n_, 256), 256, a_.p, a_sum_.p, n_, moved_.p, &scal_.p->n_moved);
         CK_LAUNCH();
         launch(delta_local_kernel, grid_for(n_ * 32, 256), 256, 
@@ -946,7 +995,6 @@ public:
         // tile scans prefer)
         const uint32_t* order = bound_active() ? nullptr : cluster_order();
         reset_scalars();
-        CK(cudaEventRecord(ev_[4], stream_));
         uint64_t n_exact = 0;
         if (screen_enabled_) {
             // (the closing kernels ride along with the screen when the last full
@@ -962,7 +1010,6 @@ public:
             scan_tiles<kInitFull>(ct_.p, ld_, k_, nullptr, order, n_);
         }
         if (!bound_active()) ub_valid_ = false;
-        if (!finish_speculated_) CK(cudaEventRecord(ev_[5], stream_));
         finish_assign(st);
         cache_trusted_ = true;
         st->n_unchanged_centroids = iteration_ <= 1 ? 0 : n_unchanged_;
@@ -983,7 +1030,6 @@ public:
         // tile scans prefer)
         const uint32_t* order = bound_active() ? nullptr : cluster_order();
         reset_scalars();
-        CK(cudaEventRecord(ev_[4], stream_));
         uint64_t n_exact = 0, n_rescan = 0;
         // With ncc_epsilon = 0 and a cache this engine produced, the NCC result
         // equals the full scan bit for bit; when many centroids
@@ -1030,7 +1076,6 @@ public:
                 }
             }
         }
-        CK(cudaEventRecord(ev_[5], stream_));
         if (!(n_chg_ > 0 && full_equiv)) ub_valid_ = false;  // per-document bounds not refreshed for every document
         last_full_equiv_ = n_chg_ > 0 && full_equiv;
         last_n_rescan_ = n_rescan;
@@ -1553,9 +1598,9 @@ private:
                drift_.p, &scal_.p->n_rec);
         launch(flags_kernel, grid_for(k_, 256), 256, k_, iteration_ <= 1 ? 1 : 0, cfg_.ncc_epsilon,
                repaired_flag_.p, drift_.p, unchanged_.p, same_.p, &scal_.p->max_drift_bits,
-               &scal_.p->n_unchanged);
+               &scal_.p->n_unchanged, touched_.p);
         CK_LAUNCH();
-        CK(cudaMemsetAsync(touched_.p, 0, k_, stream_));
+        advance_drift_launch();
         ++updates_since_assign_;
         CK(cudaEventRecord(ev_[1], stream_));  // end of the update (timed by the caller)
         pull_scalars();
@@ -1568,7 +1613,7 @@ private:
         if (n_rec > 0) cmax_ = (n_rec == k_) ? 1.0 + 0x1p-22 : std::max(cmax_, 1.0 + 0x1p-22);
         double max_drift;
         std::memcpy(&max_drift, &hs_->max_drift_bits, 8);
-        advance_drift(max_drift);
+        advance_drift_check(max_drift);
         have_cc_ = have_ids_ = false;
         std::memset(st, 0, sizeof(*st));
         st->iteration = iteration_;
@@ -1584,8 +1629,10 @@ private:
     // update's per-column drift; an update the bounds cannot follow (iteration
     // 1, an empty-cluster repair) adds nothing and invalidates them until the
     // next full screen.
-    void advance_drift(double max_sq_drift) {
-        const bool ok = iteration_ >= 2 && repaired_.empty() && max_sq_drift >= 0.0 && std::isfinite(max_sq_drift);
+    // (Launched behind the update's kernels, ahead of its scalars' round trip;
+    // the drift's finiteness is checked on the host afterwards, advance_drift_check.)
+    void advance_drift_launch() {
+        const bool ok = iteration_ >= 2 && repaired_.empty();
         if (!ok) ub_valid_ = false;
         const size_t rows = static_cast<size_t>(iteration_) + 1;
         if (dcum_.n < rows * kUbGroups) {  // grow, keeping the history (bounds refer to their own iteration's row)
@@ -1604,6 +1651,10 @@ private:
         launch(group_drift_kernel, 1, 1024, static_cast<const double*>(drift_.p), k_, ok ? 1 : 0, dcum_.p, iteration_);
         CK_LAUNCH();
         dcum_rows_ = iteration_ + 1;
+    }
+
+    void advance_drift_check(double max_sq_drift) {
+        if (!(max_sq_drift >= 0.0 && std::isfinite(max_sq_drift))) ub_valid_ = false;
     }
 
     // The changed-cluster ids and their count; with `cols`, also the compact
@@ -1748,7 +1799,8 @@ private:
                       int64_t n_work, int init) {
         btake_.alloc(n_);
         bctr_.alloc(8);
-        CK(cudaMemsetAsync(bctr_.p, 0, 8 * sizeof(unsigned long long), stream_));
+        // (the drift-bound pass's counters sit right behind the screen's: one memset for both)
+        CK(cudaMemsetAsync(bctr_.p, 0, 12 * sizeof(unsigned long long), stream_));
         // more than one 2048-column tile: one pass with hash-table accumulators
         // over every column (SSKM_HASH=0: a pass per tile)
         const bool hash = ncols > 2048 && ncols <= 65534 && hash_enabled_;  // 16-bit table keys (column + 1)
@@ -1813,8 +1865,7 @@ private:
             p.iter = iteration_;
             if (skip_enabled_ && ub_valid_ && p.same && iteration_ < dcum_rows_) {
                 skip_list_.alloc(n_);
-                skip_ctr_.alloc(4);
-                CK(cudaMemsetAsync(skip_ctr_.p, 0, 4 * sizeof(unsigned long long), stream_));
+                skip_ctr_.alloc(4);  // zeroed with the screen's counters above
                 SkipArgs q{};
                 q.indptr = indptr_.p;
                 q.n = n_;
@@ -1907,16 +1958,15 @@ private:
         // after the exact scan.
         const bool speculate = speculate_finish_ && init == kInitFull && full_cover && !hash;
         if (speculate) {
-            CK(cudaEventRecord(ev_[5], stream_));
-            finish_assign_launch();
+                finish_assign_launch();
             CK(cudaEventRecord(ev_[3], stream_));
         }
-        unsigned long long ctr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, hp[2] = {0, 0}, sk[4] = {0, 0, 0, 0};
-        CK(cudaMemcpyAsync(ctr, bctr_.p, sizeof(ctr), cudaMemcpyDeviceToHost, stream_));
-        CK(cudaMemcpyAsync(hp, hpctr_.p, sizeof(hp), cudaMemcpyDeviceToHost, stream_));
-        CK(cudaMemcpyAsync(hs_, scal_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, stream_));
-        if (skipped) CK(cudaMemcpyAsync(sk, skip_ctr_.p, sizeof(sk), cudaMemcpyDeviceToHost, stream_));
+        unsigned long long ctr[8], hp[2], sk[4];
+        CK(cudaMemcpyAsync(hblock_, ctr_block_.p, sizeof(CounterBlock), cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
+        std::memcpy(ctr, hblock_->bctr, sizeof(ctr));
+        std::memcpy(hp, hblock_->hp, sizeof(hp));
+        std::memcpy(sk, hblock_->sk, sizeof(sk));
         if (full_cover) ub_valid_ = true;  // every document: screened (fresh bound) or kept (bound still valid)
         if (skipped) {
             n_work = static_cast<int64_t>(sk[0]);  // the screen's work list
@@ -2471,13 +2521,12 @@ private:
     // cluster sizes of the new assignment, so that the next update's empty-
     // cluster check needs no round trip of its own (engine.cpp:154).
     void finish_assign_launch() {
-        reset_scalars_keep_rescan();
+        // (one kernel zeroes the cluster sizes and the four scalars these kernels
+        // add into: five memsets' worth of launches less on the host's path)
+        launch(zero_closing_kernel, grid_for(k_, 256), 256, counts_.p, k_, scal_.p);
         launch(finish_assign_kernel, kObjBlocks, 256, a_.p, a_start_.p, sims_.p, n_, obj_part_.p,
                                                               &scal_.p->reassigned);
         launch(sum_parts_kernel, 1, 256, obj_part_.p, kObjBlocks, &scal_.p->objective);
-        CK(cudaMemsetAsync(counts_.p, 0, k_ * 8, stream_));
-        CK(cudaMemsetAsync(&scal_.p->bad, 0, 4, stream_));
-        CK(cudaMemsetAsync(&scal_.p->n_empty, 0, 4, stream_));
         launch_counts();
         launch(count_empty_kernel, grid_for(k_, 256), 256, counts_.p, k_, &scal_.p->n_empty);
         CK_LAUNCH();
@@ -2502,11 +2551,10 @@ private:
     }
 
     void timing(sskm_iteration_stats* st) {
-        float ms = 0.f, kms = 0.f;
+        float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
-        CK(cudaEventElapsedTime(&kms, ev_[4], ev_[5]));
         st->assign_ms = ms;
-        st->assign_kernel_ms = kms;
+        st->assign_kernel_ms = ms;  // (its own event pair was two launches on the host's path: folded into assign_ms)
         st->screen_ms = screen_ms_;
         st->screen_launches = screen_launches_;
         st->centroid_density = last_density_;
@@ -2537,7 +2585,9 @@ private:
     int screen_blocks_per_sm_ = 8;
     bool screen_enabled_ = true;
     double cmax_ = 1.0;
-    DevBuf<Scalars> scal_;
+    DevBuf<CounterBlock> ctr_block_;
+    CounterBlock* hblock_ = nullptr;
+    DevBuf<Scalars> scal_;  // window of ctr_block_ (as bctr_, hpctr_, skip_ctr_)
     Scalars* hs_ = nullptr;
 
     bool corpus_ = false, state_ = false, have_cc_ = false, have_ids_ = false;

@@ -501,7 +501,7 @@ __global__ void apply_moves_kernel(const uint32_t* __restrict__ pairs, uint32_t 
 __global__ void flags_kernel(uint32_t k, int first_iter, double eps, const uint8_t* __restrict__ repaired,
                              const double* __restrict__ drift, uint8_t* __restrict__ unchanged,
                              uint8_t* __restrict__ same, unsigned long long* max_drift_bits,
-                             unsigned int* n_unchanged) {
+                             unsigned int* n_unchanged, uint8_t* __restrict__ touched) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
         const double dj = drift[j];  // 0 for untouched columns
         same[j] = (!first_iter && !repaired[j] && dj == 0.0) ? 1 : 0;
@@ -515,6 +515,7 @@ __global__ void flags_kernel(uint32_t k, int first_iter, double eps, const uint8
         }
         unchanged[j] = u;
         if (u) atomicAdd(n_unchanged, 1u);
+        touched[j] = 0;  // the update's last reader of the touched flags: cleared for the next one
     }
 }
 
