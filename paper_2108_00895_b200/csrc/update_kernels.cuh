@@ -276,7 +276,10 @@ __global__ void compact_ids_kernel(const uint8_t* __restrict__ flags, uint32_t k
     if (threadIdx.x == 0) *n_out = base;
 }
 
-constexpr int kRowBlock = 512;  // rows per partial in the column reductions
+#ifndef SSKM_ROW_BLOCK
+#define SSKM_ROW_BLOCK 128  // measured on c1 (update ms): 512 -> 0.457, 256 -> 0.437, 128 -> 0.412, 64 -> 0.422, 32 -> 0.466
+#endif
+constexpr int kRowBlock = SSKM_ROW_BLOCK;  // rows per partial in the column reductions
 
 // Rewrite of the touched columns: c = S · (1/‖S‖) in fp64, stored fp32, with
 // the squared drift against the previous fp32 column as fixed-order partials.
